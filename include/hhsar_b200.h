@@ -1,0 +1,234 @@
+/*
+ * hhsar_b200.h -- C ABI of the B200-native HHFFBPA / BPA hot path.
+ *
+ * Every entry point takes caller-owned DEVICE buffers (plain pointers and
+ * sizes; complex values are interleaved float32 re/im = complex64), a CUDA
+ * stream handle (cudaStream_t passed as void*), and returns an int status:
+ * 0 = OK, 1 = bad argument, 2 = CUDA error (hhsar_last_error() has text).
+ * Calls are asynchronous on the given stream; nothing synchronises except
+ * where noted.  No C++ exceptions cross the ABI and the library keeps no
+ * global state besides the last-error string (thread-local).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/hhsar):
+ *   hhsar_bp_gather        <- _kernels.backproject_gather   (_kernels.py:98-110)
+ *   hhsar_lattice_interp   <- _kernels.lattice_interpolate  (_kernels.py:354-378)
+ *   hhsar_invert_newton    <- _kernels._invert_newton_jit    (_kernels.py:255-351,
+ *                             called via spectrum.invert_lattice, spectrum.py:327-407)
+ *   hhsar_bpa_cartesian    <- bpa.bpa_reconstruct's meshgrid + backproject
+ *                             (bpa.py:163-176)
+ *   hhsar_range_demod      <- rangecomp.range_compress's pad + demodulation
+ *                             (rangecomp.py:86-96; the IDFT itself is cuFFT)
+ *   hhsar_leaf_boxes / hhsar_grid_plan / hhsar_grid_newton
+ *                          <- ffbp.build_subimage_grid for every subarray of
+ *                             every level at once (ffbp.py:179-307) plus the
+ *                             leaf delay mask of ffbp.level1_reconstruct
+ *                             (ffbp.py:320-335)
+ *   hhsar_leaf_bp          <- ffbp.level1_reconstruct's backproject
+ *                             (ffbp.py:336-340) fused with _downconvert_samples
+ *                             (ffbp.py:343-348)
+ *   hhsar_merge_level      <- ffbp.merge_pair / _merge_onto_points for every
+ *                             parent of a level (ffbp.py:351-412), and the final
+ *                             Cartesian landing (ffbp.py:493-495)
+ *   hhsar_simulate         <- simulator.simulate_measurement (simulator.py:41-69)
+ */
+#ifndef HHSAR_B200_H
+#define HHSAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HHSAR_OK 0
+#define HHSAR_EINVAL 1
+#define HHSAR_ECUDA 2
+
+/* Geometry constants shared by the grid, leaf and merge kernels.  Host code
+ * computes every derived constant in float64 exactly as the reference does
+ * (e.g. c_uv = k_max / pi, c_nhi = k_max / (2 * 2pi)) so the lattice bounds
+ * built on the device are bit-identical to the reference's. */
+typedef struct hhsar_geom {
+    double region[6];   /* x_min, x_max, y_min, y_max, z_min, z_max          */
+    double center[3];   /* region.center                                       */
+    double k_min, k_max;
+    double c_uv;        /* k_max / pi                 (spectrum.py:268, 271)   */
+    double c_nhi;       /* k_max / (2 * TWO_PI)       (spectrum.py:256)        */
+    double c_nlo;       /* k_min / (2 * TWO_PI)                                */
+    double step;        /* 1 / gamma                  (ffbp.py:241)            */
+    double margin;      /*                            (ffbp.py:269)            */
+    double max_step;    /* 0.5 * region.diagonal      (ffbp.py:260)            */
+    double tol;         /* Newton max-norm tolerance  (ffbp.py:182)            */
+    double z_floor;     /* 1e-4                       (spectrum.py:331)        */
+    double window_hi;   /* profile window upper bound [s] (rangecomp.py:56-58) */
+    int32_t pad;        /* lattice pad steps (src_pad, ffbp.py:468)            */
+    int32_t max_iter;   /* Newton iteration cap (50)                           */
+} hhsar_geom;
+
+/* One subimage lattice.  Filled by hhsar_grid_plan (bounds, dims, masks'
+ * index ranges) except start/stop/leaf range (host) and offset/col_offset
+ * (host prefix sums once dims are known). */
+typedef struct hhsar_grid_desc {
+    double ext[4];       /* lateral element bbox x_min,x_max,y_min,y_max       */
+    double box[6];       /* 3-D element bbox: lo xyz, hi xyz                   */
+    double lo[3], hi[3]; /* (u,v,n) image of the region's 5^3 boundary lattice */
+    double origin[3];    /* (u,v,n) of lattice index 0                         */
+    double slack_lo[3];  /* containment bounds region_min - slack              */
+    double slack_hi[3];  /*                    region_max + slack              */
+    int32_t dims[3];     /* nu, nv, nn                                         */
+    int32_t near_lo[3];  /* index range of the two-ring band (ffbp.py:294-301) */
+    int32_t near_hi[3];
+    int32_t core_lo[3];  /* index range of the region image (ffbp.py:302-304)  */
+    int32_t core_hi[3];
+    int32_t is_leaf;     /* apply the level-1 delay-window mask                */
+    int64_t start, stop; /* element slice [start, stop)                        */
+    int64_t leaf_lo, leaf_hi; /* leaf index range [leaf_lo, leaf_hi)           */
+    int64_t offset;      /* first lattice point in the level pools             */
+    int64_t col_offset;  /* first (u, v) column in the Newton work list        */
+} hhsar_grid_desc;
+
+/* Per-grid counters written by hhsar_grid_newton (int64 each):
+ * [0] valid points, [1] valid core points   (SubimageGrid built, ffbp.py:305)
+ * [2] valid after the leaf delay mask, [3] core valid after it (ffbp.py:331-335)
+ * [4] Newton iterations executed, [5] domain errors (rad <= gap*1e-12)       */
+#define HHSAR_GRID_STATS 6
+
+const char *hhsar_last_error(void);
+int hhsar_version(void);
+int hhsar_device_sm_count(void);
+/* Host-only: writes sizeof/offsetof facts of the structs above into out[0..n)
+ * (sizeof geom, sizeof grid_desc, offsets of geom.window_hi, geom.pad,
+ * desc.dims, desc.is_leaf, desc.start, desc.offset, desc.col_offset) and
+ * returns how many facts exist.  Lets a binding verify its struct mirrors. */
+int hhsar_abi_layout(int64_t *out, int n);
+
+/* ---- operator level ---------------------------------------------------- */
+
+/* backproject_gather: out[n] (complex64), oow[n] = count of element delays
+ * outside [0, n_t-1] samples (skipped). points/el_pos float64 [.,3]. */
+int hhsar_bp_gather(const double *points, int64_t n, const double *el_pos, int64_t m,
+                    const void *envelopes, int64_t n_t, double t0, double dt,
+                    double k_ref, void *out, int64_t *oow, void *stream);
+
+/* lattice_interpolate: values complex64 [nu][nv][nn], coords float64 [n,3]
+ * (lattice-index units) -> out complex64 [n], ok uint8 [n]; kernel 0 =
+ * linear, 1 = cubic (Keys a = -1/2).  Out-of-hull points give 0, ok = 0. */
+int hhsar_lattice_interp(const void *values, int64_t nu, int64_t nv, int64_t nn,
+                         const double *coords, int64_t n, int kernel, void *out,
+                         uint8_t *ok, void *stream);
+
+/* _invert_newton_jit: float64 targets/guesses [n,3] -> pos [n,3], ok, iters. */
+int hhsar_invert_newton(const double *ext4, double k_min, double k_max,
+                        const double *targets, const double *guesses, int64_t n,
+                        double tol, int max_iter, double max_step, double z_floor,
+                        double *pos, uint8_t *ok, int64_t *iters, void *stream);
+
+/* ---- direct BPA --------------------------------------------------------- */
+
+/* Full-aperture BPA on the region_grid voxels (values[nx][ny][nz], z
+ * fastest).  Only flattened voxels [vox_begin, vox_end) are computed and
+ * written to out[0 .. vox_end - vox_begin) (voxel sharding; vox_end < 0
+ * means "to the end").  origin/step/dims are HOST arrays.  el_xyz: float32
+ * [m][4] (x, y, z, unused).  oow_total: one int64 accumulated with the
+ * number of out-of-window point-element delays. */
+int hhsar_bpa_cartesian(const double *origin, const double *step, const int64_t *dims,
+                        int64_t vox_begin, int64_t vox_end, const float *el_xyz, int64_t m, const void *envelopes,
+                        int64_t n_t, double t0, double dt, double k_ref,
+                        void *out, int64_t *oow_total, void *stream);
+
+/* ---- range compression -------------------------------------------------- */
+
+/* Zero-pad cube[n_el][n_f] (complex64) into spec[n_el][n_t]. */
+int hhsar_range_pad(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
+                    void *spec, void *stream);
+/* In place: prof[e][i] *= scale * exp(j * a * (dt * i)) with a = (k_min -
+ * k_ref) * c (float64 phase per bin, rangecomp.py:94-96); turns the
+ * unnormalised IDFT into demodulated envelopes. */
+int hhsar_range_demod(void *prof, int64_t n_el, int64_t n_t, double a, double dt,
+                      float scale, void *stream);
+
+/* ---- HHFFBPA: grids ------------------------------------------------------ */
+
+/* 3-D bbox of every leaf's elements: el_pos float64 [N][3], bounds int64
+ * [n_leaves+1] -> box float64 [n_leaves][6]. */
+int hhsar_leaf_boxes(const double *el_pos, const int64_t *bounds, int64_t n_leaves,
+                     double *box, void *stream);
+
+/* Lattice metadata of n_grids grids (ffbp.py:226-304 without the Newton
+ * part).  boundary: float64 [n_b][3] (region.boundary_lattice(5)).  status
+ * (int32, device) receives 1 if any boundary point is outside the
+ * compressed-coordinate domain (spectrum.py:253-255).  grids, leaf_box,
+ * boundary, status are device pointers; geom is a HOST pointer (as in every
+ * call taking an hhsar_geom). */
+int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_box,
+                    const double *boundary, int64_t n_b, const hhsar_geom *geom,
+                    int32_t *status, void *stream);
+
+/* Newton inversion of every near-band (u, v) column of every grid, warm
+ * started along n (ffbp.py:271-282), then the containment, near-band and
+ * (leaf grids) delay-window masks.  positions float64 [P][3], valid uint8
+ * [P] (P = sum of lattice sizes, at desc.offset), stats int64
+ * [n_grids][HHSAR_GRID_STATS] (zeroed by the caller).  n_cols = total
+ * columns (sum nu*nv, at desc.col_offset). */
+int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_cols,
+                      const hhsar_geom *geom, double *positions, uint8_t *valid,
+                      int64_t *stats, void *stream);
+
+/* ---- HHFFBPA: leaf BPA and merges ----------------------------------------- */
+
+/* Level-1 subimages: for every valid lattice point of every leaf grid,
+ * backproject the leaf's elements [desc.start, desc.stop) and store the value
+ * at values[desc.offset + i] (complex64; masked points get 0).  With
+ * downconvert != 0 the stored value is f * exp(-j Phi_leaf(pos)), ready for
+ * the next merge (ffbp.py:343-348).  positions/valid/values are the global
+ * lattice pools indexed by desc.offset.  el_xyz float32 [N][4].  oow_total
+ * accumulates out-of-window point-element delays. */
+int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, const double *positions,
+                  const uint8_t *valid, const float *el_xyz, const void *envelopes,
+                  int64_t n_t, double t0, double dt, double k_ref, const hhsar_geom *geom,
+                  int downconvert, void *values, int64_t *oow_total, void *stream);
+
+/* One merge stage over the global lattice pools.  Parents: parent_grids
+ * [n_parents] whose points are contiguous from parent_grids[0].offset
+ * (n_parent_points in total); parent p merges children [p*fanout,
+ * (p+1)*fanout) of child_grids, whose DOWNCONVERTED values are read from
+ * values_in.  For each valid parent point: sum over children of
+ * interp(f'_c at llt_c(p)) * exp(+j Phi_c(p)); zeroed and counted in
+ * *flagged when outside any child's hull (ffbp.py:351-374).  With
+ * downconvert != 0 the result is stored times exp(-j Phi_parent(p)).
+ * kernel 0 linear, 1 cubic.  geom is a HOST pointer. */
+int hhsar_merge_level(const hhsar_grid_desc *parent_grids, int64_t n_parents,
+                      int64_t n_parent_points, const double *positions, const uint8_t *valid,
+                      const hhsar_grid_desc *child_grids, int64_t n_child_grids, int fanout,
+                      const void *values_in, const hhsar_geom *geom, int kernel,
+                      int downconvert, void *values_out, int64_t *flagged, void *stream);
+
+/* In place values[i] *= exp(-j Phi_grid(pos_i)) on valid points, 0 on masked
+ * ones, for the points of grids[0..n_grids) (contiguous from grids[0].offset);
+ * _downconvert_samples (ffbp.py:343-348) for the single-merge API. */
+int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_points,
+                      const double *positions, const uint8_t *valid, const hhsar_geom *geom,
+                      void *values, void *stream);
+
+/* Final landing on the Cartesian region_grid voxels [nx][ny][nz] (z
+ * fastest), all n_children children, no downconversion (ffbp.py:493-495).
+ * Voxels [vox_begin, vox_end) of the flattened volume are written to
+ * out[0 .. vox_end - vox_begin) (voxel sharding across GPUs). */
+int hhsar_merge_cartesian(const double *origin, const double *step, const int64_t *dims,
+                          int64_t vox_begin, int64_t vox_end,
+                          const hhsar_grid_desc *child_grids, int64_t n_children,
+                          const void *child_values, const hhsar_geom *geom, int kernel,
+                          void *out, int64_t *flagged, void *stream);
+
+/* ---- input synthesis ------------------------------------------------------ */
+
+/* Born cube s[e][f] = sum_q refl_q exp(-2j k_f |el_e - pos_q|) (complex64
+ * out; float64 phases).  refl complex128 [n_s]. */
+int hhsar_simulate(const double *el_pos, int64_t n_el, const double *pos,
+                   const double *refl, int64_t n_s, const double *k, int64_t n_f,
+                   void *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HHSAR_B200_H */

@@ -1,0 +1,416 @@
+// Subimage lattice construction for every subarray of every level in two
+// launches (reference: ffbp.py:179-307 build_subimage_grid, the Newton loop
+// _kernels.py:255-351, and the leaf delay mask ffbp.py:320-335).
+//
+// hhsar_grid_plan: one CTA per grid.  Element bbox from the leaf boxes, the
+// 125-point boundary map, and every integer decision of the lattice (counts,
+// u/v trimming, near band, core box) in bit-exact float64 (no FMA, same
+// operation order as numpy), so dims/origin/masks equal the reference's.
+//
+// hhsar_grid_newton: one thread per (u, v) column, marching along n with the
+// reference's warm starts (ffbp.py:274-282).  Columns outside the near band
+// are skipped (all their points are masked whatever Newton returns) and the
+// march stops after the last near plane -- exact pruning, SURVEY G3.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace hhsar {
+
+constexpr int PLAN_THREADS = 128;
+
+// ---- damped Newton (_kernels.py:255-351) ------------------------------------
+struct NewtonGeom {
+    double ext[4];
+    double gap, c_uv, c_nhi, c_nlo;
+};
+
+__device__ __forceinline__ bool newton_solve(const NewtonGeom &G, double tu, double tv, double tn,
+                                             double &x, double &y, double &z, double tol,
+                                             int max_iter, double max_step, double z_floor,
+                                             int &iters) {
+    const double xmn = G.ext[0], xmx = G.ext[1], ymn = G.ext[2], ymx = G.ext[3];
+    bool good = false;
+    int it;
+    for (it = 1; it <= max_iter; ++it) {
+        const double x0 = fmin(fmax(x, xmn), xmx);
+        const double y0 = fmin(fmax(y, ymn), ymx);
+        const double z2 = z * z;
+        const double ax = x - xmn, bx = x - xmx, ay = y - ymn, by = y - ymx;
+        const double yy = (y - y0) * (y - y0), xx = (x - x0) * (x - x0);
+        const double du1 = sqrt(ax * ax + yy + z2), du2 = sqrt(bx * bx + yy + z2);
+        const double dv1 = sqrt(xx + ay * ay + z2), dv2 = sqrt(xx + by * by + z2);
+        const double e1 = sqrt(ax * ax + ay * ay + z2), e2 = sqrt(ax * ax + by * by + z2);
+        const double e3 = sqrt(bx * bx + ay * ay + z2), e4 = sqrt(bx * bx + by * by + z2);
+        const double r = e1 + e2 + e3 + e4;
+        const double rad = r * r - G.gap;
+        if (rad <= 0.0 || fmin(fmin(du1, du2), fmin(dv1, dv2)) == 0.0 ||
+            fmin(fmin(e1, e2), fmin(e3, e4)) == 0.0)
+            break;
+        const double sq = sqrt(rad);
+        const double ru = G.c_uv * (du1 - du2) - tu;
+        const double rv = G.c_uv * (dv1 - dv2) - tv;
+        const double rn = G.c_nhi * sq - G.c_nlo * r - tn;
+        if (fmax(fabs(ru), fmax(fabs(rv), fabs(rn))) <= tol) {
+            good = true;
+            break;
+        }
+        const double i1 = 1.0 / du1, i2 = 1.0 / du2, i3 = 1.0 / dv1, i4 = 1.0 / dv2;
+        const double ja = G.c_uv * (ax * i1 - bx * i2);
+        const double jb = G.c_uv * ((y - y0) * i1 - (y - y0) * i2);
+        const double jc = G.c_uv * (z * i1 - z * i2);
+        const double jd = G.c_uv * ((x - x0) * i3 - (x - x0) * i4);
+        const double je = G.c_uv * (ay * i3 - by * i4);
+        const double jf = G.c_uv * (z * i3 - z * i4);
+        const double fac = G.c_nhi * (r / sq) - G.c_nlo;
+        const double f1 = 1.0 / e1, f2 = 1.0 / e2, f3 = 1.0 / e3, f4 = 1.0 / e4;
+        const double jg = fac * (ax * f1 + ax * f2 + bx * f3 + bx * f4);
+        const double jh = fac * (ay * f1 + by * f2 + ay * f3 + by * f4);
+        const double ji = fac * (z * (f1 + f2 + f3 + f4));
+        const double m0 = je * ji - jf * jh, m1 = jd * ji - jf * jg, m2 = jd * jh - je * jg;
+        const double det = ja * m0 - jb * m1 + jc * m2;
+        if (fabs(det) < 1e-30) break;
+        const double idet = 1.0 / det;
+        double sx = (ru * m0 - jb * (rv * ji - jf * rn) + jc * (rv * jh - je * rn)) * idet;
+        double sy = (ja * (rv * ji - jf * rn) - ru * m1 + jc * (jd * rn - rv * jg)) * idet;
+        double sz = (ja * (je * rn - rv * jh) - jb * (jd * rn - rv * jg) + ru * m2) * idet;
+        if (max_step > 0.0) {
+            const double sn = sqrt(sx * sx + sy * sy + sz * sz);
+            if (sn > max_step) {
+                const double sc = max_step / sn;
+                sx *= sc;
+                sy *= sc;
+                sz *= sc;
+            }
+        }
+        x -= sx;
+        y -= sy;
+        z -= sz;
+        if (z < z_floor) z = z_floor;
+    }
+    iters = it > max_iter ? max_iter : it;
+    return good;
+}
+
+// ---- leaf boxes ----------------------------------------------------------------
+template <int N>
+__device__ void block_minmax(double (&mn)[N], double (&mx)[N]) {
+    __shared__ double s_mn[N][PLAN_THREADS / 32], s_mx[N][PLAN_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fmin(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+        if (lane == 0) {
+            s_mn[k][wid] = mn[k];
+            s_mx[k][wid] = mx[k];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        mn[k] = s_mn[k][0];
+        mx[k] = s_mx[k][0];
+        for (int w = 1; w < PLAN_THREADS / 32; ++w) {
+            mn[k] = fmin(mn[k], s_mn[k][w]);
+            mx[k] = fmax(mx[k], s_mx[k][w]);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS)
+leaf_boxes_kernel(const double *__restrict__ el, const int64_t *__restrict__ bounds,
+                  double *__restrict__ box) {
+    const int64_t l = blockIdx.x;
+    double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int64_t i = bounds[l] + threadIdx.x; i < bounds[l + 1]; i += PLAN_THREADS)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = fmin(mn[a], el[3 * i + a]);
+            mx[a] = fmax(mx[a], el[3 * i + a]);
+        }
+    block_minmax<3>(mn, mx);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            box[6 * l + a] = mn[a];
+            box[6 * l + 3 + a] = mx[a];
+        }
+}
+
+// ---- lattice plan (ffbp.py:226-304) ---------------------------------------------
+__global__ void __launch_bounds__(PLAN_THREADS)
+grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__ leaf_box,
+                 const double *__restrict__ boundary, int n_b, hhsar_geom g,
+                 int32_t *__restrict__ status) {
+    hhsar_grid_desc &D = grids[blockIdx.x];
+    // element bbox over the grid's leaves (exact: min/max)
+    double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int64_t l = D.leaf_lo + threadIdx.x; l < D.leaf_hi; l += PLAN_THREADS)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = fmin(mn[a], leaf_box[6 * l + a]);
+            mx[a] = fmax(mx[a], leaf_box[6 * l + 3 + a]);
+        }
+    block_minmax<3>(mn, mx);
+    const double ext[4] = {mn[0], mx[0], mn[1], mx[1]};
+    // forward map of the region's boundary lattice -> lo, hi (ffbp.py:237-240)
+    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    bool bad = false;
+    for (int i = threadIdx.x; i < n_b; i += PLAN_THREADS) {
+        double uvn[3];
+        bad |= !llt_exact(ext, g, boundary[3 * i], boundary[3 * i + 1], boundary[3 * i + 2], uvn);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = fmin(lo[a], uvn[a]);
+            hi[a] = fmax(hi[a], uvn[a]);
+        }
+    }
+    if (bad) atomicExch(status, 1);
+    block_minmax<3>(lo, hi);
+    if (threadIdx.x != 0) return;
+
+    const double step = g.step;
+    const double padstep = xmul((double)g.pad, step);
+    double origin[3];
+    int cnt[3];
+    for (int a = 0; a < 3; ++a) {
+        origin[a] = xsub(lo[a], padstep);
+        cnt[a] = (int)ceil(xdiv(xsub(hi[a], lo[a]), step)) + 1 + 2 * g.pad;
+    }
+    // u/v trimming (ffbp.py:248-257)
+    const double limit[2] = {xmul(g.c_uv, xsub(ext[1], ext[0])), xmul(g.c_uv, xsub(ext[3], ext[2]))};
+    for (int a = 0; a < 2; ++a) {
+        const double thr = xadd(limit[a], xmul(2.0, step));
+        int first = -1, last = -1;
+        for (int i = 0; i < cnt[a]; ++i) {
+            const double plane = xadd(origin[a], xmul(step, (double)i));
+            if (fabs(plane) < thr) {
+                if (first < 0) first = i;
+                last = i;
+            }
+        }
+        const bool any = first >= 0, all = any && first == 0 && last == cnt[a] - 1 &&
+                                           (last - first + 1) == cnt[a];
+        // "all" must also mean no gap; keep is contiguous (|plane| is unimodal)
+        if (any && !all) {
+            origin[a] = xadd(origin[a], xmul((double)first, step));
+            cnt[a] = last - first + 1;
+        }
+    }
+    const double rlo[3] = {g.region[0], g.region[2], g.region[4]};
+    const double rhi[3] = {g.region[1], g.region[3], g.region[5]};
+    const double eps = xmul(1e-9, step);
+    const double two_step = xmul(2.0, step);
+    for (int a = 0; a < 3; ++a) {
+        const double extent = xsub(rhi[a], rlo[a]);
+        // shadow = 3.0 * GRID_PAD * step * extent / max(hi - lo, 1e-12)
+        const double shadow = xdiv(xmul(xmul(6.0, step), extent), fmax(xsub(hi[a], lo[a]), 1e-12));
+        const double slack = xadd(xmul(g.margin, extent), shadow);
+        D.slack_lo[a] = xsub(rlo[a], slack);
+        D.slack_hi[a] = xadd(rhi[a], slack);
+        const double near_a = xsub(xsub(lo[a], two_step), eps);
+        const double near_b = xadd(xadd(hi[a], two_step), eps);
+        const double img_a = xsub(lo[a], eps), img_b = xadd(hi[a], eps);
+        int n0 = -1, n1 = -2, c0 = -1, c1 = -1;
+        for (int i = 0; i < cnt[a]; ++i) {
+            const double t = xadd(origin[a], xmul(step, (double)i));
+            if (t >= near_a && t <= near_b) {
+                if (n0 < 0) n0 = i;
+                n1 = i;
+            }
+            if (t >= img_a && t <= img_b) {
+                if (c0 < 0) c0 = i;
+                c1 = i;
+            }
+        }
+        if (n0 < 0) n0 = 0;            // empty band: lo > hi
+        if (c0 < 0) { c0 = 0; c1 = cnt[a] - 1; }  // np.argmax of all-False
+        D.near_lo[a] = n0;
+        D.near_hi[a] = n1;
+        D.core_lo[a] = c0;
+        D.core_hi[a] = c1;
+        D.origin[a] = origin[a];
+        D.dims[a] = cnt[a];
+        D.lo[a] = lo[a];
+        D.hi[a] = hi[a];
+        D.box[a] = mn[a];
+        D.box[3 + a] = mx[a];
+    }
+    for (int k = 0; k < 4; ++k) D.ext[k] = ext[k];
+}
+
+// ---- Newton columns -------------------------------------------------------------
+__device__ __forceinline__ int find_grid(const hhsar_grid_desc *__restrict__ grids, int n,
+                                         int64_t key, bool by_col) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {  // last grid whose start <= key
+        const int mid = (lo + hi + 1) >> 1;
+        const int64_t s = by_col ? grids[mid].col_offset : grids[mid].offset;
+        if (s <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(128)
+grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
+                   hhsar_geom g, double *__restrict__ positions, uint8_t *__restrict__ valid,
+                   int64_t *__restrict__ stats) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    const int gi = find_grid(grids, n_grids, c, true);
+    const hhsar_grid_desc &D = grids[gi];
+    const int nu = D.dims[0], nv = D.dims[1], nn = D.dims[2];
+    const int64_t col = c - D.col_offset;
+    const int iu = (int)(col / nv), iv = (int)(col % nv);
+    uint8_t *vcol = valid + D.offset + col * nn;
+    double *pcol = positions + 3 * (D.offset + col * nn);
+    (void)nu;
+    unsigned n_pre = 0, core_pre = 0, n_post = 0, core_post = 0, its = 0;
+    const bool near_col = iu >= D.near_lo[0] && iu <= D.near_hi[0] && iv >= D.near_lo[1] &&
+                          iv <= D.near_hi[1];
+    const int w_end = near_col ? D.near_hi[2] + 1 : 0;
+    if (near_col && w_end > 0) {
+        NewtonGeom G;
+        for (int k = 0; k < 4; ++k) G.ext[k] = D.ext[k];
+        G.gap = box_gap_exact(D.ext);
+        G.c_uv = g.c_uv;
+        G.c_nhi = g.c_nhi;
+        G.c_nlo = g.c_nlo;
+        const double tu = xadd(D.origin[0], xmul(g.step, (double)iu));
+        const double tv = xadd(D.origin[1], xmul(g.step, (double)iv));
+        const bool core_uv = iu >= D.core_lo[0] && iu <= D.core_hi[0] && iv >= D.core_lo[1] &&
+                             iv <= D.core_hi[1];
+        double gx = g.center[0], gy = g.center[1], gz = g.center[2];
+        for (int w = 0; w < w_end; ++w) {
+            const double tn = xadd(D.origin[2], xmul(g.step, (double)w));
+            double x = gx, y = gy, z = gz > g.z_floor ? gz : g.z_floor;
+            int it = 0;
+            const bool ok = newton_solve(G, tu, tv, tn, x, y, z, g.tol, g.max_iter, g.max_step,
+                                         g.z_floor, it);
+            its += it;
+            uint8_t v = 0;
+            if (w >= D.near_lo[2]) {
+                bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] && y >= D.slack_lo[1] &&
+                           y <= D.slack_hi[1] && z >= D.slack_lo[2] && z <= D.slack_hi[2];
+                bool post = pre;
+                if (pre && D.is_leaf) {
+                    // 2 * max corner distance / c <= window_hi (ffbp.py:320-330)
+                    double dmax = 0.0;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const double cx = (b & 4) ? D.box[3] : D.box[0];
+                        const double cy = (b & 2) ? D.box[4] : D.box[1];
+                        const double cz = (b & 1) ? D.box[5] : D.box[2];
+                        const double d = xsqrt(xadd(xadd(xsq(xsub(x, cx)), xsq(xsub(y, cy))),
+                                                    xsq(xsub(z, cz))));
+                        dmax = fmax(dmax, d);
+                    }
+                    post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
+                }
+                const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
+                n_pre += pre;
+                core_pre += pre && in_core;
+                n_post += post;
+                core_post += post && in_core;
+                v = post;
+                if (pre) {
+                    pcol[3 * w] = x;
+                    pcol[3 * w + 1] = y;
+                    pcol[3 * w + 2] = z;
+                }
+            }
+            vcol[w] = v;
+            if (ok) {
+                gx = x;
+                gy = y;
+                gz = z;
+            } else {
+                gx = g.center[0];
+                gy = g.center[1];
+                gz = g.center[2];
+            }
+        }
+    }
+    for (int w = w_end; w < nn; ++w) vcol[w] = 0;
+    int64_t *st = stats + (int64_t)gi * HHSAR_GRID_STATS;
+    if (n_pre) atomicAdd((unsigned long long *)(st + 0), (unsigned long long)n_pre);
+    if (core_pre) atomicAdd((unsigned long long *)(st + 1), (unsigned long long)core_pre);
+    if (n_post) atomicAdd((unsigned long long *)(st + 2), (unsigned long long)n_post);
+    if (core_post) atomicAdd((unsigned long long *)(st + 3), (unsigned long long)core_post);
+    if (its) atomicAdd((unsigned long long *)(st + 4), (unsigned long long)its);
+}
+
+__global__ void invert_newton_kernel(NewtonGeom G, const double *__restrict__ t,
+                                     const double *__restrict__ gs, int64_t n, double tol,
+                                     int max_iter, double max_step, double z_floor,
+                                     double *__restrict__ pos, uint8_t *__restrict__ ok,
+                                     int64_t *__restrict__ iters) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double gz = gs[3 * i + 2] > z_floor ? gs[3 * i + 2] : z_floor;
+    double x = gs[3 * i], y = gs[3 * i + 1], z = gz;
+    int it = 0;
+    const bool good = newton_solve(G, t[3 * i], t[3 * i + 1], t[3 * i + 2], x, y, z, tol, max_iter,
+                                   max_step, z_floor, it);
+    iters[i] = it;
+    ok[i] = good;
+    pos[3 * i] = good ? x : gs[3 * i];
+    pos[3 * i + 1] = good ? y : gs[3 * i + 1];
+    pos[3 * i + 2] = good ? z : gz;
+}
+
+}  // namespace hhsar
+
+using namespace hhsar;
+
+extern "C" int hhsar_leaf_boxes(const double *el_pos, const int64_t *bounds, int64_t n_leaves,
+                                double *box, void *stream) {
+    HHSAR_REQUIRE(n_leaves > 0 && n_leaves < (1ll << 31), "leaf_boxes: bad leaf count");
+    leaf_boxes_kernel<<<(unsigned)n_leaves, PLAN_THREADS, 0, as_stream(stream)>>>(el_pos, bounds, box);
+    return check_launch("leaf_boxes_kernel");
+}
+
+extern "C" int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_box,
+                               const double *boundary, int64_t n_b, const hhsar_geom *geom,
+                               int32_t *status, void *stream) {
+    HHSAR_REQUIRE(n_grids > 0 && n_grids < (1ll << 31), "grid_plan: bad grid count");
+    HHSAR_REQUIRE(n_b > 0 && geom != nullptr, "grid_plan: bad boundary lattice");
+    HHSAR_REQUIRE(geom->step > 0.0 && geom->step <= 1.0, "grid_plan: step must lie in (0, 1]");
+    grid_plan_kernel<<<(unsigned)n_grids, PLAN_THREADS, 0, as_stream(stream)>>>(
+        grids, leaf_box, boundary, (int)n_b, *geom, status);
+    return check_launch("grid_plan_kernel");
+}
+
+extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_cols,
+                                 const hhsar_geom *geom, double *positions, uint8_t *valid,
+                                 int64_t *stats, void *stream) {
+    HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
+    if (n_cols == 0) return HHSAR_OK;
+    grid_newton_kernel<<<(unsigned)((n_cols + 127) / 128), 128, 0, as_stream(stream)>>>(
+        grids, (int)n_grids, n_cols, *geom, positions, valid, stats);
+    return check_launch("grid_newton_kernel");
+}
+
+extern "C" int hhsar_invert_newton(const double *ext4, double k_min, double k_max,
+                                   const double *targets, const double *guesses, int64_t n,
+                                   double tol, int max_iter, double max_step, double z_floor,
+                                   double *pos, uint8_t *ok, int64_t *iters, void *stream) {
+    HHSAR_REQUIRE(n >= 0 && max_iter >= 1, "invert_newton: bad arguments");
+    if (n == 0) return HHSAR_OK;
+    NewtonGeom G;
+    for (int k = 0; k < 4; ++k) G.ext[k] = ext4[k];
+    G.gap = 4.0 * (ext4[1] - ext4[0]) * (ext4[1] - ext4[0]) +
+            4.0 * (ext4[3] - ext4[2]) * (ext4[3] - ext4[2]);
+    const double pi = 3.141592653589793;
+    G.c_uv = k_max / pi;
+    G.c_nhi = k_max / (4.0 * pi);
+    G.c_nlo = k_min / (4.0 * pi);
+    invert_newton_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
+        G, targets, guesses, n, tol, max_iter, max_step > 0 ? max_step : 0.0, z_floor, pos, ok,
+        iters);
+    return check_launch("invert_newton_kernel");
+}

@@ -1,0 +1,310 @@
+// Level-1 subimages and the merge stages (reference: ffbp.py:310-412 and
+// ffbp.py:493-495; interpolation _kernels.py:117-200).
+//
+// Leaf BPA: one CTA per (leaf grid, slice); the leaf's elements are staged in
+// shared memory and every valid lattice point sums them (same unit as the
+// direct BPA), then the epilogue applies the leaf's spatial downconversion
+// exp(-j Phi(pos)) (ffbp.py:343-348) so the stored lattice is ready to be
+// interpolated by the next level.
+//
+// Merge: one thread per parent lattice point (or Cartesian voxel).  For every
+// child: compressed coordinates (float64), lattice interpolation of the
+// child's downconverted complex64 values, and one combined phase
+// exp(j (Phi_child(p) - Phi_parent(p))) -- re-modulation by the child and
+// downconversion for the next level in a single float64 difference.
+#include "common.cuh"
+
+namespace hhsar {
+
+constexpr int LEAF_THREADS = 256;
+constexpr int LEAF_CHUNK = 512;
+constexpr int MERGE_THREADS = 128;
+
+struct LeafConst {
+    float inv_bin, x0, rev, xmax;
+    int n_t;
+};
+
+__device__ __forceinline__ int find_by_offset(const hhsar_grid_desc *__restrict__ grids, int n,
+                                              int64_t key) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (grids[mid].offset <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(LEAF_THREADS)
+leaf_bp_kernel(const hhsar_grid_desc *__restrict__ grids, int slices,
+               const double *__restrict__ positions, const uint8_t *__restrict__ valid,
+               const float4 *__restrict__ el, const float2 *__restrict__ env, LeafConst k,
+               hhsar_geom g, int downconvert, float2 *__restrict__ values,
+               int64_t *__restrict__ oow_total) {
+    __shared__ float4 s_el[LEAF_CHUNK];
+    const hhsar_grid_desc &D = grids[blockIdx.x / slices];
+    const int slice = blockIdx.x % slices;
+    const int64_t npts = (int64_t)D.dims[0] * D.dims[1] * D.dims[2];
+    const int64_t e0 = D.start, m = D.stop - D.start;
+    const double gap = box_gap_exact(D.ext);
+    unsigned bad = 0;
+    for (int64_t base = (int64_t)slice * LEAF_THREADS; base < npts;
+         base += (int64_t)slices * LEAF_THREADS) {
+        const int64_t i = base + threadIdx.x;
+        const bool live = i < npts && valid[D.offset + i];
+        double px = 0, py = 0, pz = 0;
+        if (live) {
+            px = positions[3 * (D.offset + i)];
+            py = positions[3 * (D.offset + i) + 1];
+            pz = positions[3 * (D.offset + i) + 2];
+        }
+        const float fx = (float)px, fy = (float)py, fz = (float)pz;
+        float2 acc = make_float2(0.f, 0.f);
+        for (int64_t c0 = 0; c0 < m; c0 += LEAF_CHUNK) {
+            const int cn = (int)min((int64_t)LEAF_CHUNK, m - c0);
+            __syncthreads();
+            for (int j = threadIdx.x; j < cn; j += LEAF_THREADS) s_el[j] = el[e0 + c0 + j];
+            __syncthreads();
+            if (live)
+                for (int j = 0; j < cn; ++j) {
+                    const float4 e = s_el[j];
+                    const float dx = fx - e.x, dy = fy - e.y, dz = fz - e.z;
+                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    const float x = fmaf(d, k.inv_bin, -k.x0);
+                    if (!(x >= 0.f && x <= k.xmax)) { ++bad; continue; }
+                    const int ib = min((int)x, k.n_t - 2);
+                    const float f = x - (float)ib;
+                    const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
+                    const float2 v0 = __ldg(row + ib), v1 = __ldg(row + ib + 1);
+                    const float er = fmaf(f, v1.x - v0.x, v0.x), ei = fmaf(f, v1.y - v0.y, v0.y);
+                    const float rv = d * k.rev;
+                    float s, cc;
+                    __sincosf(6.283185307f * __fsub_rn(rv, rintf(rv)), &s, &cc);
+                    acc.x = fmaf(er, cc, fmaf(-ei, s, acc.x));
+                    acc.y = fmaf(er, s, fmaf(ei, cc, acc.y));
+                }
+        }
+        if (i < npts) {
+            float2 outv = make_float2(0.f, 0.f);
+            if (live) {
+                outv = acc;
+                if (downconvert) {
+                    const double phi = sdc_phase_fast(D.ext, gap, g.k_min, g.k_max, px, py, pz);
+                    outv = cmul(acc, cis_reduced(-phi));
+                }
+            }
+            values[D.offset + i] = outv;
+        }
+    }
+    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
+}
+
+template <int KERNEL>
+__device__ __forceinline__ bool merge_point(const hhsar_grid_desc *__restrict__ kids, int nk,
+                                            const float2 *__restrict__ kv, const hhsar_geom &g,
+                                            double x, double y, double z, double phi_parent,
+                                            float2 &acc) {
+    acc = make_float2(0.f, 0.f);
+    bool good = true;
+    for (int c = 0; c < nk; ++c) {
+        const hhsar_grid_desc &C = kids[c];
+        const double gap = box_gap_exact(C.ext);
+        const LltPhase L = llt_phase(C.ext, gap, g.c_uv, g.c_nhi, g.c_nlo, g.k_min, g.k_max, x, y, z);
+        const double cu = (L.u - C.origin[0]) / g.step;
+        const double cv = (L.v - C.origin[1]) / g.step;
+        const double cn = (L.n - C.origin[2]) / g.step;
+        float2 s;
+        const bool ok = lattice_sample<KERNEL>(kv + C.offset, C.dims[0], C.dims[1], C.dims[2], cu,
+                                               cv, cn, s);
+        good &= ok;
+        if (ok) cfma(acc, s, cis_reduced(L.phi - phi_parent));
+    }
+    if (!good) acc = make_float2(0.f, 0.f);
+    return good;
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(MERGE_THREADS)
+merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, int64_t n_points,
+                   const double *__restrict__ positions, const uint8_t *__restrict__ valid,
+                   const hhsar_grid_desc *__restrict__ kids, int fanout,
+                   const float2 *__restrict__ kv, hhsar_geom g, int downconvert,
+                   float2 *__restrict__ out, int64_t *__restrict__ flagged) {
+    const int64_t base = parents[0].offset;
+    const int64_t i = base + (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
+    if (i >= base + n_points) return;
+    unsigned fl = 0;
+    if (valid[i]) {
+        const int p = find_by_offset(parents, n_parents, i);
+        const hhsar_grid_desc &P = parents[p];
+        const double x = positions[3 * i], y = positions[3 * i + 1], z = positions[3 * i + 2];
+        const double phi_p =
+            downconvert ? sdc_phase_fast(P.ext, box_gap_exact(P.ext), g.k_min, g.k_max, x, y, z)
+                        : 0.0;
+        float2 acc;
+        fl = !merge_point<KERNEL>(kids + (int64_t)p * fanout, fanout, kv, g, x, y, z, phi_p, acc);
+        out[i] = acc;
+    } else {
+        out[i] = make_float2(0.f, 0.f);
+    }
+    warp_add(flagged, fl);
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(MERGE_THREADS)
+merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx,
+                       int ny, int nz, int64_t vb, int64_t ve,
+                       const hhsar_grid_desc *__restrict__ kids, int nk,
+                       const float2 *__restrict__ kv, hhsar_geom g, float2 *__restrict__ out,
+                       int64_t *__restrict__ flagged) {
+    const int64_t v = vb + (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
+    if (v >= ve) return;
+    const int iz = (int)(v % nz), iy = (int)((v / nz) % ny), ix = (int)(v / ((int64_t)nz * ny));
+    (void)nx;
+    const double x = __dadd_rn(ox, __dmul_rn(sx, (double)ix));
+    const double y = __dadd_rn(oy, __dmul_rn(sy, (double)iy));
+    const double z = __dadd_rn(oz, __dmul_rn(sz, (double)iz));
+    float2 acc;
+    const unsigned fl = !merge_point<KERNEL>(kids, nk, kv, g, x, y, z, 0.0, acc);
+    out[v - vb] = acc;
+    warp_add(flagged, fl);
+}
+
+template <int KERNEL>
+__global__ void lattice_interp_kernel(const float2 *__restrict__ vals, int nu, int nv, int nn,
+                                      const double *__restrict__ coords, int64_t n,
+                                      float2 *__restrict__ out, uint8_t *__restrict__ ok) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float2 s;
+    ok[i] = lattice_sample<KERNEL>(vals, nu, nv, nn, coords[3 * i], coords[3 * i + 1],
+                                   coords[3 * i + 2], s);
+    out[i] = s;
+}
+
+// values[i] *= exp(-j Phi_grid(pos_i)) for valid points, 0 elsewhere
+// (_downconvert_samples, ffbp.py:343-348) -- used by the single-merge API.
+__global__ void downconvert_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
+                                   int64_t n_points, const double *__restrict__ positions,
+                                   const uint8_t *__restrict__ valid, hhsar_geom g,
+                                   float2 *__restrict__ values) {
+    const int64_t base = grids[0].offset;
+    const int64_t i = base + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= base + n_points) return;
+    if (!valid[i]) {
+        values[i] = make_float2(0.f, 0.f);
+        return;
+    }
+    const hhsar_grid_desc &D = grids[find_by_offset(grids, n_grids, i)];
+    const double phi = sdc_phase_fast(D.ext, box_gap_exact(D.ext), g.k_min, g.k_max,
+                                      positions[3 * i], positions[3 * i + 1], positions[3 * i + 2]);
+    values[i] = cmul(values[i], cis_reduced(-phi));
+}
+
+}  // namespace hhsar
+
+using namespace hhsar;
+
+extern "C" int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, const double *positions,
+                             const uint8_t *valid, const float *el_xyz, const void *envelopes,
+                             int64_t n_t, double t0, double dt, double k_ref,
+                             const hhsar_geom *geom, int downconvert, void *values,
+                             int64_t *oow_total, void *stream) {
+    HHSAR_REQUIRE(n_grids > 0 && n_grids < (1 << 24) && geom, "leaf_bp: bad grid count");
+    HHSAR_REQUIRE(n_t >= 2, "leaf_bp: n_t must be >= 2");
+    LeafConst k;
+    k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
+    k.x0 = (float)(t0 / dt);
+    k.rev = (float)(k_ref / 3.141592653589793);
+    k.xmax = (float)(n_t - 1);
+    k.n_t = (int)n_t;
+    // enough CTAs for two waves of the SMs
+    int slices = (int)((2 * sm_count() + n_grids - 1) / n_grids);
+    if (slices < 1) slices = 1;
+    if (slices > 64) slices = 64;
+    leaf_bp_kernel<<<(unsigned)(n_grids * slices), LEAF_THREADS, 0, as_stream(stream)>>>(
+        grids, slices, positions, valid, reinterpret_cast<const float4 *>(el_xyz),
+        reinterpret_cast<const float2 *>(envelopes), k, *geom, downconvert,
+        reinterpret_cast<float2 *>(values), oow_total);
+    return check_launch("leaf_bp_kernel");
+}
+
+extern "C" int hhsar_merge_level(const hhsar_grid_desc *parent_grids, int64_t n_parents,
+                                 int64_t n_parent_points, const double *positions,
+                                 const uint8_t *valid, const hhsar_grid_desc *child_grids,
+                                 int64_t n_child_grids, int fanout, const void *values_in,
+                                 const hhsar_geom *geom, int kernel, int downconvert,
+                                 void *values_out, int64_t *flagged, void *stream) {
+    HHSAR_REQUIRE(n_parents > 0 && fanout >= 1 && n_child_grids == n_parents * fanout && geom,
+                  "merge_level: children must be n_parents * fanout");
+    HHSAR_REQUIRE(kernel == 0 || kernel == 1, "merge_level: unknown interpolation kernel");
+    if (n_parent_points == 0) return HHSAR_OK;
+    const unsigned blocks = (unsigned)((n_parent_points + MERGE_THREADS - 1) / MERGE_THREADS);
+    cudaStream_t s = as_stream(stream);
+    auto kv = reinterpret_cast<const float2 *>(values_in);
+    auto out = reinterpret_cast<float2 *>(values_out);
+    if (kernel == 0)
+        merge_level_kernel<0><<<blocks, MERGE_THREADS, 0, s>>>(
+            parent_grids, (int)n_parents, n_parent_points, positions, valid, child_grids, fanout,
+            kv, *geom, downconvert, out, flagged);
+    else
+        merge_level_kernel<1><<<blocks, MERGE_THREADS, 0, s>>>(
+            parent_grids, (int)n_parents, n_parent_points, positions, valid, child_grids, fanout,
+            kv, *geom, downconvert, out, flagged);
+    return check_launch("merge_level_kernel");
+}
+
+extern "C" int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_points,
+                                 const double *positions, const uint8_t *valid,
+                                 const hhsar_geom *geom, void *values, void *stream) {
+    HHSAR_REQUIRE(n_grids > 0 && geom, "downconvert: bad arguments");
+    if (n_points == 0) return HHSAR_OK;
+    downconvert_kernel<<<(unsigned)((n_points + 255) / 256), 256, 0, as_stream(stream)>>>(
+        grids, (int)n_grids, n_points, positions, valid, *geom, reinterpret_cast<float2 *>(values));
+    return check_launch("downconvert_kernel");
+}
+extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, const int64_t *dims,
+                                     int64_t vox_begin, int64_t vox_end,
+                                     const hhsar_grid_desc *child_grids, int64_t n_children,
+                                     const void *child_values, const hhsar_geom *geom, int kernel,
+                                     void *out, int64_t *flagged, void *stream) {
+    HHSAR_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0 && n_children > 0 && geom,
+                  "merge_cartesian: bad arguments");
+    HHSAR_REQUIRE(kernel == 0 || kernel == 1, "merge_cartesian: unknown interpolation kernel");
+    const int64_t total = dims[0] * dims[1] * dims[2];
+    if (vox_end < 0 || vox_end > total) vox_end = total;
+    HHSAR_REQUIRE(vox_begin >= 0 && vox_begin <= vox_end, "merge_cartesian: bad voxel range");
+    if (vox_begin == vox_end) return HHSAR_OK;
+    const unsigned blocks = (unsigned)((vox_end - vox_begin + MERGE_THREADS - 1) / MERGE_THREADS);
+    cudaStream_t s = as_stream(stream);
+    auto kv = reinterpret_cast<const float2 *>(child_values);
+    auto o = reinterpret_cast<float2 *>(out);
+    if (kernel == 0)
+        merge_cartesian_kernel<0><<<blocks, MERGE_THREADS, 0, s>>>(
+            origin[0], origin[1], origin[2], step[0], step[1], step[2], (int)dims[0], (int)dims[1],
+            (int)dims[2], vox_begin, vox_end, child_grids, (int)n_children, kv, *geom, o, flagged);
+    else
+        merge_cartesian_kernel<1><<<blocks, MERGE_THREADS, 0, s>>>(
+            origin[0], origin[1], origin[2], step[0], step[1], step[2], (int)dims[0], (int)dims[1],
+            (int)dims[2], vox_begin, vox_end, child_grids, (int)n_children, kv, *geom, o, flagged);
+    return check_launch("merge_cartesian_kernel");
+}
+
+extern "C" int hhsar_lattice_interp(const void *values, int64_t nu, int64_t nv, int64_t nn,
+                                    const double *coords, int64_t n, int kernel, void *out,
+                                    uint8_t *ok, void *stream) {
+    HHSAR_REQUIRE(kernel == 0 || kernel == 1, "lattice_interp: unknown interpolation kernel");
+    HHSAR_REQUIRE(nu >= 2 && nv >= 2 && nn >= 2, "lattice_interp: lattice needs >= 2 samples per axis");
+    HHSAR_REQUIRE(kernel == 0 || (nu >= 4 && nv >= 4 && nn >= 4),
+                  "lattice_interp: cubic needs >= 4 samples per axis");
+    if (n == 0) return HHSAR_OK;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    cudaStream_t s = as_stream(stream);
+    auto v = reinterpret_cast<const float2 *>(values);
+    auto o = reinterpret_cast<float2 *>(out);
+    if (kernel == 0)
+        lattice_interp_kernel<0><<<blocks, 256, 0, s>>>(v, (int)nu, (int)nv, (int)nn, coords, n, o, ok);
+    else
+        lattice_interp_kernel<1><<<blocks, 256, 0, s>>>(v, (int)nu, (int)nv, (int)nn, coords, n, o, ok);
+    return check_launch("lattice_interp_kernel");
+}

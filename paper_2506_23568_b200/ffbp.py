@@ -1,0 +1,580 @@
+"""HHFFBPA on the GPU: the drop-in for hhsar.ffbp.
+
+Reference: /root/reference/pkg/src/hhsar/ffbp.py.  ``hhffbpa_reconstruct``
+keeps its signature, provenance keys and exceptions.  The reference's Python
+loops over subarrays (ffbp.py:470-492) become a fixed sequence of batched
+launches on one stream:
+
+  1. hhsar_leaf_boxes + hhsar_grid_plan -- lattice metadata of EVERY grid of
+     EVERY level at once (bit-exact float64), then one device->host copy of
+     the small descriptors to size the lattice pools (the only mid-pipeline
+     synchronisation);
+  2. hhsar_grid_newton -- every (u, v) column of every grid, warm-started
+     along n, pruned to the near band, with containment / near / leaf delay
+     masks and per-grid counters;
+  3. hhsar_leaf_bp -- all leaves, downconverted on store;
+  4. hhsar_merge_level per merge stage -- all parents of a level at once;
+  5. hhsar_merge_cartesian -- the final landing on the region grid;
+then one device->host copy of the volume and counters, after which the
+reference's error checks run in the reference's order.
+
+``merge_factor`` (keyword, default 2 = the reference's binary tree) selects
+the N-ary schedule BASELINE configs 0/2/4 ask for: grids only at tree levels
+1, 1+s, 1+2s, ... (merge factor 2^s) and every merge sums 2^s children with
+the reference's N-ary _merge_onto_points (ffbp.py:351-374).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .bpa import (ImageVolume, _finish, bpa_volume_device, check_delay_window,
+                  default_grid_dims, el_f32x4, region_grid)
+from .errors import ConfigError, NumericDomainError
+from .model import (C_LIGHT, Subarray, boundary_lattice, leaf_bounds,
+                    partition_subarrays, validate_geometry)
+from .rangecomp import RangeProfileSet, range_compress
+from .spectrum import TWO_PI, SubarrayExtents
+
+GRID_PAD = 2  # ffbp.py:32
+BOUNDARY_PER_AXIS = 5  # ffbp.py:237
+
+
+def default_levels(aperture) -> int:
+    """ffbp.py:35-39: max(1, floor(log2(min(nx, ny))) - 2)."""
+    side = min(aperture.nx, aperture.ny)
+    return max(1, int(np.floor(np.log2(side))) - 2)
+
+
+@dataclass(frozen=True)
+class FfbpParams:
+    """Tuning knobs (ffbp.py:42-71), same validation."""
+
+    levels: int | None = None
+    gamma: float = 1.4
+    kernel: str = "linear"
+    margin: float = 0.25
+
+    def __post_init__(self):
+        if self.levels is not None and self.levels < 1:
+            raise ConfigError("levels must be at least 1")
+        if not self.gamma >= 1.0:
+            raise ConfigError("oversampling factor must be at least 1")
+        if self.kernel not in ("linear", "cubic"):
+            raise ConfigError(f"unknown interpolation kernel '{self.kernel}'")
+        if not 0.0 <= self.margin <= 1.0:
+            raise ConfigError("margin must lie in [0, 1]")
+
+
+def _kernel_id(kernel: str) -> int:
+    if kernel == "linear":
+        return 0
+    if kernel == "cubic":
+        return 1
+    raise ConfigError(f"unknown interpolation kernel '{kernel}'")
+
+
+# ---------------------------------------------------------------------------
+# schedule (host, O(#subarrays))
+# ---------------------------------------------------------------------------
+
+class Schedule:
+    """Which subarrays carry grids, in launch order, and the merge fan-outs.
+
+    Subarray j of 1-based tree level L covers leaves [j 2^(L-1), (j+1) 2^(L-1))
+    (model.py:383-386 pairs consecutive children).
+    """
+
+    def __init__(self, n_elements: int, levels: int, merge_factor: int = 2):
+        s = int(round(np.log2(merge_factor)))
+        if merge_factor < 2 or 2 ** s != merge_factor:
+            raise ConfigError("merge factor must be a power of two >= 2")
+        self.levels = levels
+        self.merge_factor = merge_factor
+        self.bounds = leaf_bounds(n_elements, levels)
+        self.n_leaves = len(self.bounds) - 1
+        self.grid_levels = list(range(1, levels, s)) or [1]
+        rows, self.level_slices = [], []
+        for lev in self.grid_levels:
+            span = 1 << (lev - 1)
+            lf0 = np.arange(0, self.n_leaves, span)
+            g0 = sum(len(r) for r in rows)
+            rows.append(lf0)
+            self.level_slices.append((g0, g0 + lf0.size))
+        lf0 = np.concatenate(rows)
+        span = np.concatenate([np.full(r.size, 1 << (lev - 1)) for r, lev in
+                               zip(rows, self.grid_levels)])
+        g = np.zeros(lf0.size, dtype=_native.GRID_DTYPE)
+        g["leaf_lo"] = lf0
+        g["leaf_hi"] = lf0 + span
+        g["start"] = self.bounds[lf0]
+        g["stop"] = self.bounds[lf0 + span]
+        g["is_leaf"] = span == 1
+        self.grids = g
+        # children per parent for each merge stage, and for the final landing
+        self.fanouts = [1 << (b - a) for a, b in zip(self.grid_levels[:-1], self.grid_levels[1:])]
+        last = self.level_slices[-1]
+        self.final_children = last[1] - last[0]
+
+    @property
+    def n_grids(self) -> int:
+        return self.grids.size
+
+
+def make_geom(region, kgrid, gamma: float, margin: float, pad: int, window_hi: float,
+              tol: float = 1e-9, max_iter: int = 50, z_floor: float = 1e-4) -> np.ndarray:
+    """hhsar_geom with every constant computed in float64 exactly as the
+    reference computes it (spectrum.py:256-272, ffbp.py:241-269)."""
+    k_min, k_max = kgrid.k_min, kgrid.k_max
+    extents = (region.x_max - region.x_min, region.y_max - region.y_min,
+               region.z_max - region.z_min)
+    diag = float(getattr(region, "diagonal", np.linalg.norm(extents)))
+    center = [(region.x_min + region.x_max) / 2, (region.y_min + region.y_max) / 2,
+              (region.z_min + region.z_max) / 2]
+    return _native.host_struct(_native.GEOM_DTYPE, dict(
+        region=[region.x_min, region.x_max, region.y_min, region.y_max, region.z_min,
+                region.z_max],
+        center=center, k_min=k_min, k_max=k_max, c_uv=k_max / np.pi,
+        c_nhi=k_max / (2.0 * TWO_PI), c_nlo=k_min / (2.0 * TWO_PI),
+        step=np.full(3, 1.0 / gamma)[0], margin=margin, max_step=0.5 * diag, tol=tol,
+        z_floor=z_floor, window_hi=window_hi, pad=pad, max_iter=max_iter))
+
+
+# ---------------------------------------------------------------------------
+# device lattices
+# ---------------------------------------------------------------------------
+
+class Lattices:
+    """All grids of a schedule on the device: descriptors + global pools.
+
+    Pools are indexed by desc.offset: positions float64 [P,3] (valid points
+    only are meaningful), valid uint8 [P], values complex64 [P] stored
+    downconverted, stats int64 [G,6].
+    """
+
+    def __init__(self, descs, descs_dev, positions, valid, stats, geom):
+        self.descs = descs
+        self.descs_dev = descs_dev
+        self.positions = positions
+        self.valid = valid
+        self.stats = stats
+        self.geom = geom
+        self.npts = np.prod(descs["dims"].astype(np.int64), axis=1)
+        self.values = None
+
+    def desc_ptr(self, g: int):
+        import ctypes
+        return ctypes.c_void_p(self.descs_dev.data_ptr() + int(g) * _native.GRID_DTYPE.itemsize)
+
+    def points_in(self, g0: int, g1: int) -> int:
+        return int(self.npts[g0:g1].sum())
+
+
+def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float,
+                   pad: int, window_hi: float, tol: float = 1e-9, max_iter: int = 50) -> Lattices:
+    """Plan + Newton for every grid of the schedule (ffbp.py:179-307)."""
+    import torch
+    dev = el_dev.device
+    stream = _native.stream_handle()
+    bounds = torch.as_tensor(sched.bounds, dtype=torch.int64, device=dev)
+    leaf_box = torch.empty((sched.n_leaves, 6), dtype=torch.float64, device=dev)
+    _native.call("hhsar_leaf_boxes", _native.ptr(el_dev), _native.ptr(bounds), sched.n_leaves,
+                 _native.ptr(leaf_box), stream)
+    bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
+    boundary = torch.as_tensor(bl, device=dev)
+    descs_dev = _native.device_struct(sched.grids, dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    geom = make_geom(region, kgrid, gamma, margin, pad, window_hi, tol, max_iter)
+    _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
+                 _native.ptr(boundary), bl.shape[0], _native.ptr(geom), _native.ptr(status),
+                 stream)
+    host = np.frombuffer(descs_dev.cpu().numpy().tobytes(), dtype=_native.GRID_DTYPE).copy()
+    if int(status.cpu()[0]):
+        raise NumericDomainError("compressed coordinates undefined this close to the array plane")
+    dims = host["dims"].astype(np.int64)
+    npts = dims.prod(axis=1)
+    host["offset"] = np.concatenate([[0], np.cumsum(npts)[:-1]])
+    cols = dims[:, 0] * dims[:, 1]
+    host["col_offset"] = np.concatenate([[0], np.cumsum(cols)[:-1]])
+    descs_dev.copy_(torch.from_numpy(host.view(np.uint8).reshape(-1)), non_blocking=False)
+    total = int(npts.sum())
+    positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
+    valid = torch.empty(total, dtype=torch.uint8, device=dev)
+    stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
+    _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, int(cols.sum()),
+                 _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
+                 _native.ptr(stats), stream)
+    return Lattices(host, descs_dev, positions, valid, stats, geom)
+
+
+@dataclass
+class DeviceRun:
+    """Device-side result of one HHFFBPA pass (everything still in HBM)."""
+    volume: object            # complex64 [vox_end - vox_begin]
+    lattices: Lattices
+    sched: Schedule
+    flags: object             # int64 [n_merge_stages + 1]
+    oow: object               # int64 [1]
+
+
+def hhffbpa_device(env, el_dev, el4, t0: float, dt: float, k_ref: float, kgrid, region,
+                   final_dims, params: FfbpParams, levels: int, merge_factor: int = 2,
+                   vox_range=None, window_hi=None) -> DeviceRun:
+    """The fused HHFFBPA pipeline on device-resident envelopes (levels >= 2)."""
+    import torch
+    dev = env.device
+    stream = _native.stream_handle()
+    kid = _kernel_id(params.kernel)
+    src_pad = GRID_PAD + (3 if params.kernel == "cubic" else 2)  # ffbp.py:468
+    if window_hi is None:
+        window_hi = t0 + (env.shape[1] - 1) * dt
+    sched = Schedule(el_dev.shape[0], levels, merge_factor)
+    lat = build_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin, src_pad,
+                         window_hi)
+    total = int(lat.npts.sum())
+    values = torch.empty(total, dtype=torch.complex64, device=dev)
+    lat.values = values
+    n_stages = len(sched.fanouts)
+    flags = torch.zeros(n_stages + 1, dtype=torch.int64, device=dev)
+    oow = torch.zeros(1, dtype=torch.int64, device=dev)
+    g0, g1 = sched.level_slices[0]
+    _native.call("hhsar_leaf_bp", lat.desc_ptr(g0), g1 - g0, _native.ptr(lat.positions),
+                 _native.ptr(lat.valid), _native.ptr(el4), _native.ptr(env), env.shape[1],
+                 float(t0), float(dt), float(k_ref), _native.ptr(lat.geom), 1,
+                 _native.ptr(values), _native.ptr(oow), stream)
+    for k, fan in enumerate(sched.fanouts):
+        c0, c1 = sched.level_slices[k]
+        p0, p1 = sched.level_slices[k + 1]
+        _native.call("hhsar_merge_level", lat.desc_ptr(p0), p1 - p0, lat.points_in(p0, p1),
+                     _native.ptr(lat.positions), _native.ptr(lat.valid), lat.desc_ptr(c0),
+                     c1 - c0, fan, _native.ptr(values), _native.ptr(lat.geom), kid, 1,
+                     _native.ptr(values), _native.c_void_p_offset(flags, k), stream)
+    origin, step = region_grid(region, final_dims)
+    n_vox = int(np.prod(final_dims))
+    vb, ve = vox_range if vox_range is not None else (0, n_vox)
+    vol = torch.empty(ve - vb, dtype=torch.complex64, device=dev)
+    c0, c1 = sched.level_slices[-1]
+    d = np.asarray(final_dims, dtype=np.int64)
+    _native.call("hhsar_merge_cartesian", _native.ptr(np.ascontiguousarray(origin)),
+                 _native.ptr(np.ascontiguousarray(step)), _native.ptr(d), vb, ve,
+                 lat.desc_ptr(c0), c1 - c0, _native.ptr(values), _native.ptr(lat.geom), kid,
+                 _native.ptr(vol), _native.c_void_p_offset(flags, n_stages), stream)
+    return DeviceRun(volume=vol, lattices=lat, sched=sched, flags=flags, oow=oow)
+
+
+def _core_masked(desc, n_valid_core) -> float:
+    size = int(np.prod(desc["core_hi"].astype(np.int64) - desc["core_lo"] + 1))
+    return 1.0 - (int(n_valid_core) / size)
+
+
+def _raise_core(masked: float):
+    raise NumericDomainError(
+        f"{100 * masked:.0f}% of core lattice points have no valid inverse "
+        "position; the region is incompatible with this subarray")
+
+
+def check_grids(run: DeviceRun, stats: np.ndarray):
+    """The reference's SubimageGrid health checks (ffbp.py:127-133) in the
+    reference's order: each leaf as built, then after its delay mask
+    (ffbp.py:331-335), then every parent level by level."""
+    sched, descs = run.sched, run.lattices.descs
+    g0, g1 = sched.level_slices[0]
+    for g in range(g0, g1):
+        for col in (1, 3):
+            m = _core_masked(descs[g], stats[g, col])
+            if m >= 0.5:
+                _raise_core(m)
+    for (a, b) in sched.level_slices[1:]:
+        for g in range(a, b):
+            m = _core_masked(descs[g], stats[g, 1])
+            if m >= 0.5:
+                _raise_core(m)
+
+
+def provenance_of(run: DeviceRun, stats, flags, final_dims, params, levels, upsample,
+                  merge_factor=2) -> dict:
+    sched = run.sched
+    level_points = []
+    for k, (a, b) in enumerate(sched.level_slices):
+        col = 2 if k == 0 else 0
+        level_points.append([int(v) for v in stats[a:b, col]])
+    n_final = int(np.prod(final_dims))
+    level_points.append([n_final])
+    merge_flags = [int(f) for f in flags[:-1]]
+    final_flags = int(flags[-1])
+    merged_total = sum(sum(p) for p in level_points[1:])
+    flagged_total = sum(merge_flags) + final_flags
+    prov = {"algorithm": "hhffbpa", "levels": levels, "gamma": params.gamma,
+            "kernel": params.kernel, "margin": params.margin, "upsample": upsample,
+            "dims": list(final_dims), "level_points": level_points, "merge_flags": merge_flags,
+            "final_flags": final_flags,
+            "flagged_fraction": (flagged_total / merged_total) if merged_total else 0.0}
+    if merge_factor != 2:
+        prov["merge_factor"] = merge_factor
+    return prov
+
+
+def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None = None,
+                        upsample: int = 8, *, merge_factor: int = 2) -> ImageVolume:
+    """Cartesian volume by factorised backprojection (ffbp.py:415-513)."""
+    import torch
+    if params is None:
+        params = FfbpParams()
+    validate_geometry(cube.aperture, region)
+    kgrid = cube.freqs
+    if final_dims is None:
+        final_dims = default_grid_dims(region, kgrid)
+    final_dims = tuple(int(d) for d in final_dims)
+    levels = params.levels if params.levels is not None else default_levels(cube.aperture)
+    profiles = range_compress(cube, upsample)
+    check_delay_window(profiles, region)
+    origin, step = region_grid(region, final_dims)
+    el4 = el_f32x4(profiles.elements_dev)
+    if levels == 1:  # ffbp.py:460-464: plain BPA onto the final grid
+        vol, oow = bpa_volume_device(profiles.envelopes, el4, region, final_dims, profiles.t0,
+                                     profiles.dt, profiles.k_ref)
+        n = int(np.prod(final_dims))
+        prov = {"algorithm": "hhffbpa", "levels": 1, "gamma": params.gamma,
+                "kernel": params.kernel, "margin": params.margin, "upsample": upsample,
+                "dims": list(final_dims), "level_points": [[n]], "merge_flags": [],
+                "final_flags": 0, "flagged_fraction": 0.0}
+        return _finish(vol, oow, final_dims, origin, step, prov)[0]
+    if region.z_min <= 0.0:
+        raise ConfigError("region must sit strictly in front of the array")
+    partition_subarrays(cube.aperture, levels)  # raises ConfigError when too deep
+    run = hhffbpa_device(profiles.envelopes, profiles.elements_dev, el4, profiles.t0,
+                         profiles.dt, profiles.k_ref, kgrid, region, final_dims, params, levels,
+                         merge_factor, window_hi=profiles.window[1])
+    extra = torch.cat([run.flags, run.lattices.stats.reshape(-1)])
+    volume, tail = _finish(run.volume, run.oow, final_dims, origin, step, {}, extra)
+    n_flags = run.flags.numel()
+    flags = tail[:n_flags]
+    stats = tail[n_flags:].reshape(-1, _native.GRID_STATS)
+    check_grids(run, stats)
+    prov = provenance_of(run, stats, flags, final_dims, params, levels, upsample, merge_factor)
+    object.__setattr__(volume, "provenance", prov)
+    return volume
+
+
+# ---------------------------------------------------------------------------
+# single-subimage API (build_subimage_grid, level1_reconstruct, merge_pair)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SubimageGrid:
+    """Lattice of one subarray (ffbp.py:74-158), host arrays.
+
+    Positions of masked points are not computed on the GPU (their values are
+    zero and nothing reads them); they hold the region centre.
+    """
+
+    subarray: object
+    extents: SubarrayExtents
+    origin: np.ndarray
+    step: np.ndarray
+    positions: np.ndarray
+    valid: np.ndarray
+    core: tuple | None = None
+
+    def __post_init__(self):
+        origin = np.asarray(self.origin, dtype=float).reshape(3)
+        step = np.asarray(self.step, dtype=float).reshape(3)
+        if np.any(step > 1.0 + 1e-12) or np.any(step <= 0.0):
+            raise ConfigError("lattice step must lie in (0, 1]")
+        pos = np.asarray(self.positions, dtype=float)
+        valid = np.asarray(self.valid, dtype=bool)
+        if pos.ndim != 4 or pos.shape[-1] != 3 or valid.shape != pos.shape[:3]:
+            raise ConfigError("positions must be (nu, nv, nn, 3) with a matching validity mask")
+        core = self.core
+        if core is None:
+            core = tuple((0, n - 1) for n in valid.shape)
+        else:
+            core = tuple((int(a), int(b)) for a, b in core)
+            for (a, b), n in zip(core, valid.shape):
+                if not 0 <= a <= b < n:
+                    raise ConfigError("core bounds must lie inside the lattice")
+        masked = 1.0 - valid[tuple(slice(a, b + 1) for a, b in core)].mean()
+        if masked >= 0.5:
+            _raise_core(masked)
+        for k, v in (("core", core), ("origin", origin), ("step", step), ("positions", pos),
+                     ("valid", valid)):
+            object.__setattr__(self, k, v)
+
+    @property
+    def dims(self):
+        return self.positions.shape[:3]
+
+    @property
+    def n_points(self) -> int:
+        return int(np.prod(self.dims))
+
+    @property
+    def n_valid(self) -> int:
+        return int(self.valid.sum())
+
+    @property
+    def masked_fraction(self) -> float:
+        return 1.0 - self.valid.mean()
+
+    def lattice_coords(self, uvn):
+        return (np.asarray(uvn, dtype=float) - self.origin) / self.step
+
+
+@dataclass(frozen=True)
+class Subimage:
+    """Complex samples of one subarray's partial image (ffbp.py:161-176)."""
+
+    grid: SubimageGrid
+    values: np.ndarray
+    downconverted: bool = False
+
+    def __post_init__(self):
+        v = np.asarray(self.values)
+        if not np.iscomplexobj(v):
+            v = v.astype(np.complex128)
+        if v.shape != self.grid.dims:
+            raise ConfigError(f"value shape {v.shape} does not match grid dims {self.grid.dims}")
+        if not np.all(v[~self.grid.valid] == 0.0):
+            raise ConfigError("masked lattice points must carry zero values")
+        object.__setattr__(self, "values", v)
+
+
+def _one_desc(ext, origin, dims, start, stop, offset=0):
+    d = np.zeros(1, dtype=_native.GRID_DTYPE)
+    d["ext"] = ext
+    d["origin"] = origin
+    d["dims"] = dims
+    d["start"], d["stop"], d["offset"] = start, stop, offset
+    return d
+
+
+def build_subimage_grid(aperture, subarray, region, kgrid, gamma: float = 1.4,
+                        margin: float = 0.25, tol: float = 1e-9, max_iter: int = 50,
+                        pad: int = GRID_PAD) -> SubimageGrid:
+    """One subarray's lattice (ffbp.py:179-307) through the batched kernels."""
+    import torch
+    if isinstance(aperture, SubarrayExtents) or (hasattr(aperture, "x_min") and
+                                                  not hasattr(aperture, "elements")):
+        ext = aperture if isinstance(aperture, SubarrayExtents) else SubarrayExtents(
+            aperture.x_min, aperture.x_max, aperture.y_min, aperture.y_max)
+        el = np.array([[ext.x_min, ext.y_min, 0.0], [ext.x_max, ext.y_max, 0.0]])
+    else:
+        el = np.asarray(aperture.elements, dtype=float)
+        if subarray is not None:
+            el = el[subarray.start:subarray.stop]
+        ext = SubarrayExtents(float(el[:, 0].min()), float(el[:, 0].max()),
+                              float(el[:, 1].min()), float(el[:, 1].max()))
+    if not gamma >= 1.0:
+        raise ConfigError("oversampling factor must be at least 1")
+    if region.z_min <= 0.0:
+        raise ConfigError("region must sit strictly in front of the array")
+    if int(pad) != pad or pad < 1:
+        raise ConfigError("pad must be an integer >= 1")
+    _native.library()
+    el_dev = torch.as_tensor(np.ascontiguousarray(el), device="cuda")
+    sched = Schedule(el.shape[0], 1)
+    sched.grids["is_leaf"] = 0
+    lat = build_lattices(el_dev, sched, region, kgrid, gamma, margin, int(pad), np.inf, tol,
+                         max_iter)
+    d = lat.descs[0]
+    dims = tuple(int(v) for v in d["dims"])
+    center = np.array([(region.x_min + region.x_max) / 2, (region.y_min + region.y_max) / 2,
+                       (region.z_min + region.z_max) / 2])
+    valid = lat.valid.cpu().numpy().astype(bool).reshape(dims)
+    pos = lat.positions.cpu().numpy().reshape(dims + (3,))
+    pos = np.where(valid[..., None], pos, center)
+    core = tuple((int(d["core_lo"][a]), int(d["core_hi"][a])) for a in range(3))
+    return SubimageGrid(subarray=subarray, extents=ext, origin=d["origin"].copy(),
+                        step=np.full(3, 1.0 / gamma), positions=pos, valid=valid, core=core)
+
+
+def _geom_for(kgrid, gamma=1.4):
+    return _native.host_struct(_native.GEOM_DTYPE, dict(
+        k_min=kgrid.k_min, k_max=kgrid.k_max, c_uv=kgrid.k_max / np.pi,
+        c_nhi=kgrid.k_max / (2.0 * TWO_PI), c_nlo=kgrid.k_min / (2.0 * TWO_PI),
+        step=1.0 / gamma))
+
+
+def level1_reconstruct(profiles: RangeProfileSet, subarray, grid: SubimageGrid) -> Subimage:
+    """Backproject one subarray onto its grid (ffbp.py:310-340); the delay
+    mask uses the 8 corners of the subarray's 3-D element bbox."""
+    import torch
+    flat = grid.positions.reshape(-1, 3)
+    mask = grid.valid.ravel().copy()
+    if mask.any():
+        els = np.asarray(profiles.aperture.elements)[subarray.start:subarray.stop]
+        lo, hi = els.min(axis=0), els.max(axis=0)
+        corners = np.stack([np.where(np.array(bits), hi, lo) for bits in np.ndindex(2, 2, 2)])
+        pts = flat[mask]
+        dmax = np.linalg.norm(pts[:, None, :] - corners[None], axis=2).max(axis=1)
+        mask[mask] = 2.0 * dmax / C_LIGHT <= profiles.window[1]
+    if not np.array_equal(mask, grid.valid.ravel()):
+        grid = SubimageGrid(subarray=grid.subarray, extents=grid.extents, origin=grid.origin,
+                            step=grid.step, positions=grid.positions,
+                            valid=mask.reshape(grid.dims), core=grid.core)
+    dev = profiles.envelopes.device
+    desc = _one_desc(grid.extents.as_tuple(), grid.origin, grid.dims, subarray.start,
+                     subarray.stop)
+    desc_dev = _native.device_struct(desc, dev)
+    pos = torch.as_tensor(np.ascontiguousarray(flat), device=dev)
+    val = torch.as_tensor(mask.astype(np.uint8), device=dev)
+    out = torch.empty(flat.shape[0], dtype=torch.complex64, device=dev)
+    oow = torch.zeros(1, dtype=torch.int64, device=dev)
+    geom = _geom_for(profiles.freqs, 1.0 / float(grid.step[0]))
+    _native.call("hhsar_leaf_bp", _native.ptr(desc_dev), 1, _native.ptr(pos), _native.ptr(val),
+                 _native.ptr(el_f32x4(profiles.elements_dev)), _native.ptr(profiles.envelopes),
+                 profiles.envelopes.shape[1], float(profiles.t0), float(profiles.dt),
+                 float(profiles.k_ref), _native.ptr(geom), 0, _native.ptr(out), _native.ptr(oow),
+                 _native.stream_handle())
+    bad = int(oow.cpu()[0])
+    if bad:
+        raise NumericDomainError(
+            f"{bad} point-element delays fell outside the profile window; "
+            "enlarge the upsampled profile or shrink the geometry")
+    return Subimage(grid=grid, values=out.cpu().numpy().reshape(grid.dims), downconverted=False)
+
+
+def merge_pair(a: Subimage, b: Subimage, parent_grid: SubimageGrid, kgrid,
+               kernel: str = "linear"):
+    """Merge two sibling subimages onto their parent's grid (ffbp.py:377-412)."""
+    import torch
+    kid = _kernel_id(kernel)
+    parent = parent_grid.subarray
+    if parent is not None:
+        for child in (a, b):
+            csa = child.grid.subarray
+            if csa is not None and not (parent.start <= csa.start and csa.stop <= parent.stop):
+                raise ConfigError("children must cover element slices inside the parent subarray")
+    _native.library()
+    grids = (a.grid, b.grid, parent_grid)
+    sizes = [g.n_points for g in grids]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    descs = np.concatenate([_one_desc(g.extents.as_tuple(), g.origin, g.dims, 0, 0, o)
+                            for g, o in zip(grids, offs[:-1])])
+    dev = torch.device("cuda")
+    descs_dev = _native.device_struct(descs, dev)
+    pos = torch.as_tensor(np.concatenate([g.positions.reshape(-1, 3) for g in grids]), device=dev)
+    val = torch.as_tensor(np.concatenate([g.valid.ravel() for g in grids]).astype(np.uint8),
+                          device=dev)
+    vals = np.zeros(offs[-1], dtype=np.complex64)
+    vals[:offs[2]] = np.concatenate([np.asarray(s.values).ravel() for s in (a, b)])
+    values = torch.as_tensor(vals, device=dev)
+    geom = _geom_for(kgrid, 1.0 / float(parent_grid.step[0]))
+    stream = _native.stream_handle()
+    base = descs_dev.data_ptr()
+    import ctypes
+    for k, s in enumerate((a, b)):
+        if not s.downconverted:
+            _native.call("hhsar_downconvert", ctypes.c_void_p(base + k * descs.itemsize), 1,
+                         sizes[k], _native.ptr(pos), _native.ptr(val), _native.ptr(geom),
+                         _native.ptr(values), stream)
+    flagged = torch.zeros(1, dtype=torch.int64, device=dev)
+    _native.call("hhsar_merge_level", ctypes.c_void_p(base + 2 * descs.itemsize), 1, sizes[2],
+                 _native.ptr(pos), _native.ptr(val), ctypes.c_void_p(base), 2, 2,
+                 _native.ptr(values), _native.ptr(geom), kid, 0, _native.ptr(values),
+                 _native.ptr(flagged), stream)
+    out = values[offs[2]:].cpu().numpy().reshape(parent_grid.dims)
+    return Subimage(grid=parent_grid, values=out, downconverted=False), int(flagged.cpu()[0])

@@ -1,0 +1,101 @@
+"""Range compression into device-resident complex64 envelopes.
+
+Mirrors rangecomp.range_compress (/root/reference/pkg/src/hhsar/rangecomp.py:
+61-101): an unnormalised zero-padded inverse DFT over the n_f frequency
+samples to n_t = upsample * n_f delay bins, then demodulation from the band
+start to the band-centre carrier k_ref.  The IDFT is a batched cuFFT (through
+torch.fft, norm="forward" = no 1/n factor); the demodulation is the
+hhsar_range_demod kernel (float64 phase per bin).  The result stays in HBM
+as envelopes[N_el][n_t] complex64, time fastest -- the layout every
+backprojection kernel reads.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError
+from .model import C_LIGHT
+
+
+@dataclass(frozen=True)
+class RangeProfileSet:
+    """RangeProfileSet (rangecomp.py:24-58) with device envelopes.
+
+    ``envelopes`` is a CUDA complex64 tensor [N_el, n_t]; ``elements_dev`` the
+    float64 element positions on the same device.
+    """
+
+    envelopes: object
+    t0: float
+    dt: float
+    upsample: int
+    k_ref: float
+    aperture: object
+    freqs: object
+    elements_dev: object = None
+
+    @property
+    def n_samples(self) -> int:
+        return int(self.envelopes.shape[1])
+
+    @property
+    def window(self) -> tuple:
+        return (self.t0, self.t0 + (self.n_samples - 1) * self.dt)
+
+
+def profile_axis(freqs, upsample: int):
+    """(n_t, dt, k_ref, a) exactly as rangecomp.py:84-96 computes them;
+    a = (k_min - k_ref) * c is the demodulation rate per second of delay."""
+    if int(upsample) != upsample or upsample < 1:
+        raise ConfigError("upsample factor must be an integer >= 1")
+    upsample = int(upsample)
+    k_min, k_max = freqs.k_min, freqs.k_max
+    dk = (k_max - k_min) / (freqs.count - 1)
+    n_t = upsample * freqs.count
+    dt = 2.0 * np.pi / (n_t * dk * C_LIGHT)
+    k_ref = 0.5 * (k_min + k_max)
+    return n_t, dt, k_ref, (k_min - k_ref) * C_LIGHT
+
+
+def to_device_cube(values, device="cuda", stream=None):
+    """Host complex cube -> device complex64 (pinned staging, async copy)."""
+    import torch
+    if isinstance(values, torch.Tensor):
+        return values.to(device=device, dtype=torch.complex64, non_blocking=True)
+    arr = np.ascontiguousarray(values, dtype=np.complex64)
+    host = torch.from_numpy(arr)
+    try:
+        host = host.pin_memory()
+    except RuntimeError:
+        pass
+    return host.to(device, non_blocking=True)
+
+
+def range_compress_device(cube_dev, freqs, upsample: int = 8):
+    """Device cube [N_el, n_f] complex64 -> envelopes [N_el, n_t] complex64."""
+    import torch
+    n_t, dt, k_ref, a = profile_axis(freqs, upsample)
+    prof = torch.fft.ifft(cube_dev, n=n_t, dim=1, norm="forward")
+    if prof.dtype != torch.complex64:
+        prof = prof.to(torch.complex64)
+    prof = prof.contiguous()
+    _native.call("hhsar_range_demod", _native.ptr(prof), prof.shape[0], n_t, a, dt, 1.0,
+                 _native.stream_handle())
+    return prof, dt, k_ref
+
+
+def range_compress(cube, upsample: int = 8, device="cuda") -> RangeProfileSet:
+    """range_compress (rangecomp.py:61-101) on the GPU."""
+    import torch
+    _native.library()
+    n_t, dt, k_ref, _ = profile_axis(cube.freqs, upsample)
+    cube_dev = to_device_cube(cube.values, device)
+    env, dt, k_ref = range_compress_device(cube_dev, cube.freqs, upsample)
+    el = torch.as_tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
+                         device=device)
+    return RangeProfileSet(envelopes=env, t0=0.0, dt=dt, upsample=int(upsample), k_ref=k_ref,
+                           aperture=cube.aperture, freqs=cube.freqs, elements_dev=el)

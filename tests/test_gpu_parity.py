@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the
+CPU oracle on identical seeded inputs.
+
+Bar (BASELINE.json north_star): complex-image relative L2 <= 1e-3 and an
+identical peak-voxel index; lattice metadata (dims, origin, core) and
+validity masks bit-exact; provenance counts equal.  The GPU computes in
+float32/complex64 (float64 for lattice geometry), so the measured errors sit
+around 1e-5..1e-4.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from goldens import grid_valid, load, provenance, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3  # north_star: complex-image relative L2
+
+
+@pytest.fixture(scope="module")
+def hh():
+    import paper_2506_23568_b200 as hh
+    from paper_2506_23568_b200 import _native
+    _native.library()  # fail loudly (no skip) when the CUDA library is unusable
+    return hh
+
+
+@pytest.fixture(scope="module")
+def small():
+    return load("small")
+
+
+def _peak(v):
+    v = np.abs(np.asarray(v))
+    return np.unravel_index(np.argmax(v), v.shape)
+
+
+def _peak_gap(v):
+    a = np.sort(np.abs(np.asarray(v)).ravel())
+    return float((a[-1] - a[-2]) / a[-1])
+
+
+def assert_image_parity(got, want, tol=TOL):
+    err = rel_l2(got, want)
+    assert err <= tol, f"relative L2 {err:.3e} > {tol}"
+    if _peak_gap(want) > 1e-4:
+        assert _peak(got) == _peak(want), (_peak(got), _peak(want), _peak_gap(want))
+    return err
+
+
+def test_bpa_small_vs_reference(hh, small):
+    vol = hh.bpa_reconstruct(small.cube, small.region, dims=small.dims)
+    err = assert_image_parity(vol.values, small.z["bpa"], 1e-4)
+    assert vol.provenance == {"algorithm": "bpa", "upsample": 8, "dims": list(small.dims)}
+    assert vol.values.shape == small.dims
+    print(f"bpa small rel-L2 {err:.2e}")
+
+
+def test_range_profiles_vs_reference(hh, small):
+    prof = hh.range_compress(small.cube, 8)
+    env = prof.envelopes.cpu().numpy()
+    assert rel_l2(env, small.z["envelopes"]) < 1e-5
+    t0, dt, k_ref = small.z["profile_meta"]
+    assert prof.t0 == t0 and prof.dt == dt and prof.k_ref == k_ref
+
+
+def test_backproject_probes_selections_and_empty(hh, small):
+    prof = hh.range_compress(small.cube, 8)
+    got = hh.backproject(prof, slice(None), small.z["probes"])
+    assert rel_l2(got, small.z["probe_values"]) < 1e-4
+    sub = hh.backproject(prof, hh.Subarray(10, 33), small.z["probes"])
+    assert rel_l2(sub, small.z["probe_values_sub"]) < 1e-4
+    via_idx = hh.backproject(prof, np.arange(10, 33), small.z["probes"])
+    assert rel_l2(via_idx, sub) < 1e-6
+    empty = hh.backproject(prof, slice(0, 0), small.z["probes"])
+    assert empty.shape == (40,) and np.all(empty == 0)
+
+
+def test_backproject_out_of_window_raises(hh, small):
+    prof = hh.range_compress(small.cube, 8)
+    far = np.array([[0.0, 0.0, 1e3]])
+    with pytest.raises(hh.NumericDomainError):
+        hh.backproject(prof, slice(None), far)
+
+
+@pytest.mark.parametrize("tag,levels,kernel", [("m2", 2, "linear"), ("m3", 3, "linear"),
+                                               ("m3c", 3, "cubic")])
+def test_hhffbpa_small_vs_reference(hh, small, tag, levels, kernel):
+    vol = hh.hhffbpa_reconstruct(small.cube, small.region, small.dims,
+                                 hh.FfbpParams(levels=levels, kernel=kernel))
+    err = assert_image_parity(vol.values, small.z["hh_" + tag])
+    want = provenance(small.z, "hh_" + tag)
+    p = vol.provenance
+    assert p["level_points"] == want["level_points"]
+    assert p["merge_flags"] == want["merge_flags"]
+    assert p["final_flags"] == want["final_flags"]
+    assert p["flagged_fraction"] == pytest.approx(float(small.z["hh_" + tag + "_flagged_fraction"]))
+    print(f"hhffbpa small {tag} rel-L2 {err:.2e}")
+
+
+def test_all_grid_metadata_and_masks_bit_exact(hh, small):
+    import torch
+    from paper_2506_23568_b200 import ffbp
+    sched = ffbp.Schedule(small.aperture.n_elements, 3)
+    el = torch.as_tensor(np.asarray(small.aperture.elements), device="cuda")
+    lat = ffbp.build_lattices(el, sched, small.region, small.freqs, 1.4, 0.25, 4, np.inf)
+    d = lat.descs
+    z = small.z
+    assert np.array_equal(d["dims"], z["grid_dims"])
+    assert np.array_equal(d["origin"], z["grid_origin"])
+    assert np.array_equal(np.concatenate([d["core_lo"][:, :, None], d["core_hi"][:, :, None]],
+                                         axis=2).reshape(-1, 6), z["grid_core"])
+    assert np.array_equal(d["ext"], z["grid_ext"])
+    valid = lat.valid.cpu().numpy().astype(bool)
+    want = np.concatenate([v.ravel() for v in grid_valid(z, "grid")])
+    assert np.array_equal(valid, want)
+    pos = lat.positions.cpu().numpy()
+    assert np.max(np.abs(pos[valid] - z["grid_positions"][valid])) < 1e-9
+    stats = lat.stats.cpu().numpy()
+    assert np.array_equal(stats[:, 0], z["grid_nvalid"])
+
+
+def test_build_subimage_grid_single(hh, small):
+    tree = hh.partition_subarrays(small.aperture, 3)
+    g = hh.build_subimage_grid(small.aperture, tree.levels[0][0], small.region, small.freqs,
+                               gamma=1.4)
+    assert g.dims == tuple(small.z["grid_pad2_dims"][0])
+    assert np.array_equal(g.origin, small.z["grid_pad2_origin"][0])
+    assert np.array_equal(g.valid, grid_valid(small.z, "grid_pad2")[0])
+    v = g.valid.ravel()
+    assert np.max(np.abs(g.positions.reshape(-1, 3)[v] - small.z["grid_pad2_positions"][v])) < 1e-9
+
+
+def test_unreachable_region_raises(hh, small):
+    hopeless = hh.ImagingRegion(-0.02, 0.02, -0.02, 0.02, 1e-6, 2e-6)
+    with pytest.raises(hh.NumericDomainError):
+        hh.build_subimage_grid(small.aperture, None, hopeless, small.freqs)
+
+
+def test_level1_and_merge_pair_vs_reference(hh, small):
+    prof = hh.range_compress(small.cube, 8)
+    tree = hh.partition_subarrays(small.aperture, 3)
+    grids = [hh.build_subimage_grid(small.aperture, sa, small.region, small.freqs, 1.4, 0.25,
+                                    pad=4) for lvl in tree.levels[:2] for sa in lvl]
+    leaves = [hh.level1_reconstruct(prof, sa, g) for sa, g in zip(tree.levels[0], grids[:4])]
+    got = np.concatenate([l.values.ravel() for l in leaves])
+    assert rel_l2(got, small.z["leaf_values"]) < 1e-4
+    valid = np.unpackbits(small.z["leaf_valid"])[:got.size].astype(bool)
+    assert np.array_equal(np.concatenate([l.grid.valid.ravel() for l in leaves]), valid)
+    merged, flagged = hh.merge_pair(leaves[0], leaves[1], grids[4], small.freqs)
+    assert rel_l2(merged.values, small.z["merge01"]) < 1e-4
+    assert flagged == int(small.z["merge01_flagged"])
+    with pytest.raises(hh.ConfigError):
+        hh.merge_pair(leaves[0], leaves[2], grids[4], small.freqs)
+
+
+@pytest.mark.parametrize("kernel", ["linear", "cubic"])
+def test_lattice_interpolate_operator(hh, small, kernel):
+    from paper_2506_23568_b200 import _kernels
+    v, ok = _kernels.lattice_interpolate(small.z["interp_lattice"], small.z["interp_coords"],
+                                         kernel)
+    assert np.array_equal(ok, small.z[f"interp_{kernel}_ok"])
+    assert np.max(np.abs(v - small.z[f"interp_{kernel}"])) < 1e-5
+
+
+def test_newton_operator(hh, small):
+    from paper_2506_23568_b200 import _kernels
+    z = small.z
+    e = z["newton_ext"]
+    pos, ok, it = _kernels.invert_newton(e[0], e[1], e[2], e[3], small.freqs.k_min,
+                                         small.freqs.k_max, z["newton_targets"],
+                                         z["newton_guesses"], 1e-9, 50,
+                                         float(z["newton_max_step"]), 1e-4)
+    assert np.array_equal(ok, z["newton_ok"])
+    assert np.max(np.abs(pos[ok] - z["newton_pos"][ok])) < 1e-9
+
+
+def test_medium_vs_reference(hh):
+    m = load("medium")
+    vol = hh.bpa_reconstruct(m.cube, m.region, dims=m.dims)
+    assert_image_parity(vol.values, m.z["bpa"], 1e-4)
+    for lv in (3, 4):
+        vol = hh.hhffbpa_reconstruct(m.cube, m.region, m.dims, hh.FfbpParams(levels=lv))
+        assert_image_parity(vol.values, m.z[f"hh_m{lv}"])
+        assert vol.provenance["level_points"] == provenance(m.z, f"hh_m{lv}")["level_points"]
+
+
+@pytest.fixture(scope="module")
+def config0():
+    return load("config0")
+
+
+def test_config0_bpa(hh, config0):
+    vol = hh.bpa_reconstruct(config0.cube, config0.region, dims=config0.dims, upsample=8)
+    err = assert_image_parity(vol.values, config0.z["bpa"])
+    print(f"config0 bpa rel-L2 {err:.2e}, peak gap {_peak_gap(config0.z['bpa']):.3e}")
+
+
+@pytest.mark.parametrize("tag,factor", [("m7", 2), ("f4", 4)])
+def test_config0_hhffbpa(hh, config0, tag, factor):
+    vol = hh.hhffbpa_reconstruct(config0.cube, config0.region, config0.dims,
+                                 hh.FfbpParams(levels=7), upsample=8, merge_factor=factor)
+    err = assert_image_parity(vol.values, config0.z["hh_" + tag])
+    want = provenance(config0.z, "hh_" + tag)
+    assert vol.provenance["level_points"] == want["level_points"]
+    assert vol.provenance["merge_flags"] == want["merge_flags"]
+    assert vol.provenance["final_flags"] == want["final_flags"]
+    print(f"config0 hhffbpa {tag} rel-L2 {err:.2e}")
+
+
+def test_config0_all_grid_masks(hh, config0):
+    import torch
+    from paper_2506_23568_b200 import ffbp
+    sched = ffbp.Schedule(config0.aperture.n_elements, 7)
+    el = torch.as_tensor(np.asarray(config0.aperture.elements), device="cuda")
+    lat = ffbp.build_lattices(el, sched, config0.region, config0.freqs, 1.4, 0.25, 4, np.inf)
+    z = config0.z
+    assert np.array_equal(lat.descs["dims"], z["grid_dims"])
+    assert np.array_equal(lat.descs["origin"], z["grid_origin"])
+    valid = lat.valid.cpu().numpy().astype(bool)
+    want = np.concatenate([v.ravel() for v in grid_valid(z, "grid")])
+    assert int((valid != want).sum()) == 0
+
+
+def test_single_level_equals_bpa(hh, small):
+    a = hh.hhffbpa_reconstruct(small.cube, small.region, small.dims, hh.FfbpParams(levels=1))
+    b = hh.bpa_reconstruct(small.cube, small.region, dims=small.dims)
+    assert np.array_equal(a.values, b.values)
+    assert a.provenance["level_points"] == [[int(np.prod(small.dims))]]
+
+
+def test_linearity(hh, small):
+    from paper_2506_23568_b200.model import DataCube
+    rng = np.random.default_rng(4)
+    shape = small.cube.values.shape
+    other = (rng.normal(size=shape) + 1j * rng.normal(size=shape)).astype(np.complex64)
+    base = np.asarray(small.cube.values, dtype=np.complex64)
+    params = hh.FfbpParams(levels=2)
+    dims = (17, 17, 9)
+    va = hh.hhffbpa_reconstruct(small.cube, small.region, dims, params).values
+    vb = hh.hhffbpa_reconstruct(DataCube(other, small.aperture, small.freqs), small.region,
+                                dims, params).values
+    vab = hh.hhffbpa_reconstruct(DataCube(base + other, small.aperture, small.freqs),
+                                 small.region, dims, params).values
+    assert rel_l2(vab, va + vb) < 1e-5
+
+
+def test_gpu_matches_oracle_on_config2_subset(hh):
+    """A frame-reduced config 2 (freehand MIMO, 8 virtual elements) through
+    both the GPU and the oracle, binary M=6."""
+    from paper_2506_23568_b200 import workloads
+    w = workloads.config(2, frames=256)
+    cube = workloads.simulate_numpy(w)
+    dims = (40, 40, 16)
+    g = hh.hhffbpa_reconstruct(cube, w.region, dims, hh.FfbpParams(levels=6), upsample=4)
+    o, _, _, prov = oracle.hhffbpa_reconstruct(cube, w.region, dims, levels=6, upsample=4)
+    assert_image_parity(g.values, o)
+    assert g.provenance["level_points"] == prov["level_points"]
+    assert g.provenance["merge_flags"] == prov["merge_flags"]
