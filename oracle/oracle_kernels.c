@@ -56,6 +56,29 @@ void oracle_bp_gather(const double *pts, int64_t n, const double *el, int64_t m,
     }
 }
 
+/* simulator.py:41-69 -- first-order Born cube
+ * s[e][f] = sum_q refl_q exp(-2j k_f |el_e - pos_q|), float64. */
+void oracle_simulate(const double *el, int64_t n_el, const double *pos, const double *refl,
+                     int64_t n_s, const double *k, int64_t n_f, double *out, int threads) {
+    set_threads(threads);
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_el; ++e) {
+        double *row = out + 2 * e * n_f;
+        for (int64_t f = 0; f < n_f; ++f) { row[2 * f] = 0.0; row[2 * f + 1] = 0.0; }
+        for (int64_t q = 0; q < n_s; ++q) {
+            const double dx = el[3 * e] - pos[3 * q], dy = el[3 * e + 1] - pos[3 * q + 1],
+                         dz = el[3 * e + 2] - pos[3 * q + 2];
+            const double d = sqrt(dx * dx + dy * dy + dz * dz);
+            const double rr = refl[2 * q], ri = refl[2 * q + 1];
+            for (int64_t f = 0; f < n_f; ++f) {
+                const double ph = -2.0 * k[f] * d, c = cos(ph), s = sin(ph);
+                row[2 * f] += rr * c - ri * s;
+                row[2 * f + 1] += rr * s + ri * c;
+            }
+        }
+    }
+}
+
 static void keys4(double f, double w[4]) { /* _kernels.py:192-200, a = -1/2 */
     w[0] = ((-0.5 * f + 1.0) * f - 0.5) * f;
     w[1] = (1.5 * f - 2.5) * f * f + 1.0;

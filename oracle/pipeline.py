@@ -27,7 +27,7 @@ __all__ = [
     "bp_gather", "backproject", "bpa_reconstruct", "extents_of", "sdc_phase",
     "llt_forward", "invert_newton", "interpolate", "build_grid", "level1",
     "merge_onto_points", "merge_children", "hhffbpa_reconstruct",
-    "default_grid_dims", "leaf_bounds", "tree_levels", "threads",
+    "default_grid_dims", "leaf_bounds", "tree_levels", "threads", "simulate",
 ]
 
 C_LIGHT = 299792458.0
@@ -77,6 +77,7 @@ def _native():
         lib.oracle_bp_gather.argtypes = [P, I64, P, I64, P, I64, D, D, D, P, P, I]
         lib.oracle_interp.argtypes = [P, I64, I64, I64, P, I64, I, P, P, I]
         lib.oracle_newton.argtypes = [D, D, D, D, D, D, P, P, I64, D, I, D, D, P, P, P, I]
+        lib.oracle_simulate.argtypes = [P, I64, P, P, I64, P, I64, P, I]
         lib.oracle_max_threads.restype = I
         _lib = lib
     return _lib
@@ -106,6 +107,18 @@ def bp_gather(points, el_pos, envelopes, t0, dt, k_ref):
                                    _ptr(env), env.shape[1], float(t0), float(dt),
                                    float(k_ref), _ptr(out), _ptr(oow), _THREADS)
     return out, oow
+
+
+def simulate(elements, positions, refl, k_samples):
+    """simulator.py:41-69 Born cube, complex128 [N_el, n_f]."""
+    el = np.ascontiguousarray(elements, dtype=np.float64).reshape(-1, 3)
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    r = np.ascontiguousarray(np.asarray(refl, dtype=np.complex128))
+    k = np.ascontiguousarray(k_samples, dtype=np.float64)
+    out = np.zeros((el.shape[0], k.size), dtype=np.complex128)
+    _native().oracle_simulate(_ptr(el), el.shape[0], _ptr(pos), _ptr(r), pos.shape[0],
+                              _ptr(k), k.size, _ptr(out), _THREADS)
+    return out
 
 
 def interpolate(values, coords, kernel="linear"):

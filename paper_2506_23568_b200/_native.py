@@ -161,7 +161,7 @@ def simulate(elements, positions, refl, k_samples, device="cuda"):
     rr = torch.as_tensor(r.view(np.float64), device=device)
     k = torch.as_tensor(np.ascontiguousarray(k_samples, dtype=np.float64), device=device)
     out = torch.empty((el.shape[0], k.shape[0]), dtype=torch.complex64, device=device)
-    call("hhsar_simulate", ptr(el), el.shape[0], ptr(pos), pos.shape[0], ptr(rr), pos.shape[0],
+    call("hhsar_simulate", ptr(el), el.shape[0], ptr(pos), ptr(rr), pos.shape[0],
          ptr(k), k.shape[0], ptr(out), stream_handle())
     return out
 

@@ -12,6 +12,7 @@ backprojection kernel reads.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -67,11 +68,12 @@ def to_device_cube(values, device="cuda", stream=None):
     if isinstance(values, torch.Tensor):
         return values.to(device=device, dtype=torch.complex64, non_blocking=True)
     arr = np.ascontiguousarray(values, dtype=np.complex64)
-    host = torch.from_numpy(arr)
-    try:
-        host = host.pin_memory()
-    except RuntimeError:
-        pass
+    with warnings.catch_warnings():  # read-only (frozen) arrays are only read here
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(arr)
+    if not host.is_pinned():
+        # staging copy: pageable host memory cannot be DMA'd asynchronously
+        return host.to(device)
     return host.to(device, non_blocking=True)
 
 
@@ -95,7 +97,7 @@ def range_compress(cube, upsample: int = 8, device="cuda") -> RangeProfileSet:
     n_t, dt, k_ref, _ = profile_axis(cube.freqs, upsample)
     cube_dev = to_device_cube(cube.values, device)
     env, dt, k_ref = range_compress_device(cube_dev, cube.freqs, upsample)
-    el = torch.as_tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
-                         device=device)
+    el = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
+                      device=device)
     return RangeProfileSet(envelopes=env, t0=0.0, dt=dt, upsample=int(upsample), k_ref=k_ref,
                            aperture=cube.aperture, freqs=cube.freqs, elements_dev=el)
