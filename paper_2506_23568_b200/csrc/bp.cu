@@ -43,7 +43,190 @@ __device__ __forceinline__ bool bp_unit(float d, const BpConst &k, const float2 
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Tiled Cartesian BPA (the config-1 hot kernel).
+//
+// A CTA owns a VX x TY x TZ voxel tile (each thread VX voxels along x) and
+// walks the elements in chunks.  Per chunk and element it derives the delay
+// window the whole tile can touch (point-to-box distance .. farthest box
+// corner, +-2 bins) and stages just those bins into shared memory as
+// (v_i, v_{i+1} - v_i) float4 pairs, so every unit does ONE 16-byte LDS and
+// two FMAs for the envelope interpolation.  Elements whose window is wider
+// than TW bins or touches the profile edges take a per-unit checked path
+// (global loads, exact out-of-window skip-and-count) -- a block-uniform
+// branch, so the fast path carries no per-unit bounds checks: the tile-level
+// window proves every delay is inside [0, n_t-1].
+// Floor/fraction and the carrier revolution count use the 1.5*2^23
+// round-to-integer trick on the FMA pipe (no F2I/I2F/FRND), sqrt is the SFU
+// approximation, and sin/cos take an explicitly range-reduced argument.
+// ---------------------------------------------------------------------------
+constexpr int TL_VX = 4, TL_TY = 16, TL_TZ = 16;  // 4 x 16 x 16 = 1024 voxels
+constexpr int TL_THREADS = TL_TY * TL_TZ;
+constexpr int TL_CHUNK = 64;   // elements per staging pass
+constexpr int TL_W = 32;       // staged bins per element (32 x 16 B = 512 B)
+constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+constexpr unsigned MAGIC_BITS = 0x4B400000u;
+
+struct BpFast {
+    float inv_bin, x0, rev, xmax;
+    float cbin;   // -0.5 - x0
+    float kfrac;  // MAGIC - x0
+    int n_t;
+};
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__global__ void __launch_bounds__(TL_THREADS)
+bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx, int ny,
+                int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el, int m,
+                const float2 *__restrict__ env, BpFast k, float2 *__restrict__ out,
+                int64_t *__restrict__ oow_total, int tx_base, int n_tiles, int split,
+                float2 *__restrict__ part) {
+    __shared__ float4 s_env[TL_CHUNK * TL_W];  // 32 KB
+    __shared__ float4 s_el[TL_CHUNK];          // x, y, z, bits(byte offset | -1 = slow)
+    __shared__ int s_lo[TL_CHUNK];
+    const int tiles_z = (nz + TL_TZ - 1) / TL_TZ, tiles_y = (ny + TL_TY - 1) / TL_TY;
+    // work item = (element split s, tile); all tiles of split 0 first so the
+    // concurrently resident CTAs stream the same elements (L2 reuse)
+    const int sidx = blockIdx.x / n_tiles;
+    const int b = blockIdx.x % n_tiles;
+    const int tz = b % tiles_z, ty = (b / tiles_z) % tiles_y;
+    const int tx = tx_base + b / (tiles_z * tiles_y);
+    const int per = ((m + split - 1) / split + TL_CHUNK - 1) / TL_CHUNK * TL_CHUNK;
+    const int e_begin = min(m, sidx * per), e_end = min(m, e_begin + per);
+    const int t = threadIdx.x;
+    const int iz = tz * TL_TZ + (t % TL_TZ), iy = ty * TL_TY + (t / TL_TZ), ix0 = tx * TL_VX;
+    const int izc = min(iz, nz - 1), iyc = min(iy, ny - 1);
+    // voxel coordinates exactly as numpy builds them (origin + step * i), then f32
+    const float py = (float)__dadd_rn(oy, __dmul_rn(sy, (double)iyc));
+    const float pz = (float)__dadd_rn(oz, __dmul_rn(sz, (double)izc));
+    float px[TL_VX];
+    bool live[TL_VX];
+    int64_t flat[TL_VX];
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v) {
+        const int ix = ix0 + v;
+        px[v] = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix, nx - 1)));
+        flat[v] = ((int64_t)ix * ny + iy) * nz + iz;
+        live[v] = ix < nx && iy < ny && iz < nz && flat[v] >= vb && flat[v] < ve;
+    }
+    // tile bounding box (float32, from the clamped corner voxels)
+    const float bx0 = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix0, nx - 1)));
+    const float bx1 = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix0 + TL_VX - 1, nx - 1)));
+    const float by0 = (float)__dadd_rn(oy, __dmul_rn(sy, (double)min(ty * TL_TY, ny - 1)));
+    const float by1 = (float)__dadd_rn(oy, __dmul_rn(sy, (double)min(ty * TL_TY + TL_TY - 1, ny - 1)));
+    const float bz0 = (float)__dadd_rn(oz, __dmul_rn(sz, (double)min(tz * TL_TZ, nz - 1)));
+    const float bz1 = (float)__dadd_rn(oz, __dmul_rn(sz, (double)min(tz * TL_TZ + TL_TZ - 1, nz - 1)));
+
+    float2 acc[TL_VX];
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v) acc[v] = make_float2(0.f, 0.f);
+    unsigned bad = 0;
+    const BpConst kc{k.inv_bin, k.x0, k.rev, k.xmax, k.n_t};
+
+    for (int c0 = e_begin; c0 < e_end; c0 += TL_CHUNK) {
+        const int cn = min(TL_CHUNK, e_end - c0);
+        __syncthreads();
+        if (t < cn) {
+            const float4 e = el[c0 + t];
+            const float qx = fminf(fmaxf(e.x, bx0), bx1) - e.x;
+            const float qy = fminf(fmaxf(e.y, by0), by1) - e.y;
+            const float qz = fminf(fmaxf(e.z, bz0), bz1) - e.z;
+            const float fx = fmaxf(fabsf(e.x - bx0), fabsf(e.x - bx1));
+            const float fy = fmaxf(fabsf(e.y - by0), fabsf(e.y - by1));
+            const float fz = fmaxf(fabsf(e.z - bz0), fabsf(e.z - bz1));
+            const float xlo = sqrtf(qx * qx + qy * qy + qz * qz) * k.inv_bin - k.x0;
+            const float xhi = sqrtf(fx * fx + fy * fy + fz * fz) * k.inv_bin - k.x0;
+            const int lo = max((int)floorf(xlo) - 2, 0);
+            const int hi = min((int)floorf(xhi) + 2, k.n_t - 1);
+            const bool fast = xlo >= 1.f && xhi <= k.xmax - 1.f && hi - lo + 1 <= TL_W;
+            const unsigned off = (unsigned)(t * TL_W - lo) * 16u - MAGIC_BITS * 16u;
+            s_el[t] = make_float4(e.x, e.y, e.z, __int_as_float(fast ? (int)off : -1));
+            s_lo[t] = fast ? lo : -1;
+        }
+        __syncthreads();
+        for (int q = t; q < cn * TL_W; q += TL_THREADS) {
+            const int j = q / TL_W, lo = s_lo[j];
+            if (lo < 0) continue;
+            const int bin = lo + (q % TL_W);
+            const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
+            const float2 v0 = __ldg(row + min(bin, k.n_t - 1));
+            const float2 v1 = __ldg(row + min(bin + 1, k.n_t - 1));
+            s_env[q] = bin < k.n_t - 1 ? make_float4(v0.x, v0.y, v1.x - v0.x, v1.y - v0.y)
+                                       : make_float4(v0.x, v0.y, 0.f, 0.f);
+        }
+        __syncthreads();
+        for (int j = 0; j < cn; ++j) {
+            const float4 e = s_el[j];
+            const float dy = py - e.y, dz = pz - e.z;
+            const float dyz = fmaf(dy, dy, dz * dz);
+            const int offb = __float_as_int(e.w);
+            if (offb != -1) {
+#pragma unroll
+                for (int v = 0; v < TL_VX; ++v) {
+                    const float dx = px[v] - e.x;
+                    const float d = sqrt_approx(fmaf(dx, dx, dyz));
+                    // i = round(x - 0.5) = floor(x) (x - 1 at exact integers, f = 1):
+                    // MAGIC + (x - 0.5) rounds at the units place.  (MAGIC - 0.5 is
+                    // not an fp32 number, so the 0.5 shift cannot ride in one FFMA.)
+                    const float tb = __fadd_rn(fmaf(d, k.inv_bin, k.cbin), MAGIC);
+                    // f = x - i = d * inv_bin + (MAGIC - x0 - tb): one rounding
+                    const float f = fmaf(d, k.inv_bin, __fsub_rn(k.kfrac, tb));
+                    const unsigned byte = (unsigned)__float_as_int(tb) * 16u + (unsigned)offb;
+                    const float4 w = *reinterpret_cast<const float4 *>(
+                        reinterpret_cast<const char *>(s_env) + byte);
+                    const float er = fmaf(f, w.z, w.x), ei = fmaf(f, w.w, w.y);
+                    const float r1 = fmaf(d, k.rev, MAGIC);              // MAGIC + round(revs)
+                    const float red = fmaf(d, k.rev, -__fsub_rn(r1, MAGIC));  // in [-0.5, 0.5]
+                    float s, c;
+                    __sincosf(6.2831853f * red, &s, &c);
+                    acc[v].x = fmaf(er, c, fmaf(-ei, s, acc[v].x));
+                    acc[v].y = fmaf(er, s, fmaf(ei, c, acc[v].y));
+                }
+            } else {
+                const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
+#pragma unroll
+                for (int v = 0; v < TL_VX; ++v) {
+                    const float dx = px[v] - e.x;
+                    const float d = sqrtf(fmaf(dx, dx, dyz));
+                    float2 a = acc[v];
+                    const bool ok = bp_unit(d, kc, row, a);
+                    if (live[v]) {
+                        acc[v] = a;
+                        bad += !ok;
+                    }
+                }
+            }
+        }
+    }
+    float2 *dst = sidx == 0 ? out : part + (int64_t)(sidx - 1) * (ve - vb);
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v)
+        if (live[v]) dst[flat[v] - vb] = acc[v];
+    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
+}
+
+// out[i] += part[0][i] + part[1][i] + ... (fixed order: deterministic)
+__global__ void add_parts_kernel(float2 *__restrict__ out, const float2 *__restrict__ part,
+                                 int n_parts, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 a = out[i];
+        for (int p = 0; p < n_parts; ++p) {
+            const float2 b = part[(int64_t)p * n + i];
+            a.x += b.x;
+            a.y += b.y;
+        }
+        out[i] = a;
+    }
+}
+
 // Full-aperture BPA over region_grid voxels, flattened index in [vb, ve).
+// (First version, kept for A/B comparisons: HHSAR_BPA_KERNEL=simple.)
 __global__ void __launch_bounds__(BP_THREADS)
 bpa_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx,
                      int ny, int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el,
@@ -142,6 +325,29 @@ __global__ void el_to_f32x4(const double *__restrict__ el, int64_t m, float4 *__
     if (i < m) o[i] = make_float4((float)el[3 * i], (float)el[3 * i + 1], (float)el[3 * i + 2], 0.f);
 }
 
+// Element-split factor that best fills the last wave: work items = tiles x
+// split, resident slots = SMs x CTAs/SM; pick split in [1, 8] maximising
+// items / (slots * ceil(items / slots)) (ties -> smaller split).
+int tile_split(int64_t tiles, int64_t m) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpa_tile_kernel, TL_THREADS, 0);
+        if (per_sm <= 0) per_sm = 1;
+    }
+    const double slots = (double)sm_count() * per_sm;
+    int best = 1;
+    double best_eff = 0.0;
+    for (int sp = 1; sp <= 8 && (int64_t)sp * TL_CHUNK <= m; ++sp) {
+        const double waves = tiles * (double)sp / slots;
+        const double eff = waves / ceil(waves);
+        if (eff > best_eff + 0.01) {
+            best_eff = eff;
+            best = sp;
+        }
+    }
+    return best;
+}
+
 BpConst make_bp_const(int64_t n_t, double t0, double dt, double k_ref) {
     BpConst k;
     k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
@@ -169,13 +375,51 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
     HHSAR_REQUIRE(vox_begin >= 0 && vox_begin <= vox_end, "bpa_cartesian: bad voxel range");
     if (vox_begin == vox_end) return HHSAR_OK;
     const int nx = (int)dims[0], ny = (int)dims[1], nz = (int)dims[2];
-    const int64_t tiles = (int64_t)((nx + CART_V - 1) / CART_V) * ((ny + CART_TY - 1) / CART_TY) *
-                          ((nz + CART_TZ - 1) / CART_TZ);
     cudaStream_t s = as_stream(stream);
     if (m == 0) {
         cudaMemsetAsync(out, 0, (vox_end - vox_begin) * sizeof(float2), s);
         return check_launch("bpa_cartesian memset");
     }
+    static const bool simple = [] {
+        const char *v = getenv("HHSAR_BPA_KERNEL");
+        return v && v[0] == 's';
+    }();
+    if (!simple) {
+        BpFast k;
+        const BpConst c = make_bp_const(n_t, t0, dt, k_ref);
+        k.inv_bin = c.inv_bin;
+        k.x0 = c.x0;
+        k.rev = c.rev;
+        k.xmax = c.xmax;
+        k.n_t = c.n_t;
+        k.cbin = -0.5f - c.x0;
+        k.kfrac = MAGIC - c.x0;
+        // only tiles intersecting [vox_begin, vox_end) matter; x-slab sharding
+        // keeps that a contiguous run of tile columns
+        const int64_t plane = (int64_t)ny * nz;
+        const int tx0 = (int)((vox_begin / plane) / TL_VX);
+        const int tx1 = (int)(((vox_end - 1) / plane) / TL_VX);
+        const int64_t per_x = (int64_t)((ny + TL_TY - 1) / TL_TY) * ((nz + TL_TZ - 1) / TL_TZ);
+        const int64_t tiles = (int64_t)(tx1 - tx0 + 1) * per_x;
+        const int split = tile_split(tiles, m);
+        float2 *part = nullptr;
+        const int64_t nv = vox_end - vox_begin;
+        if (split > 1 && cudaMallocAsync(&part, (split - 1) * nv * sizeof(float2), s) != cudaSuccess)
+            return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
+        bpa_tile_kernel<<<(unsigned)(tiles * split), TL_THREADS, 0, s>>>(
+            origin[0], origin[1], origin[2], step[0], step[1], step[2], nx, ny,
+            nz, vox_begin, vox_end, reinterpret_cast<const float4 *>(el_xyz), (int)m,
+            reinterpret_cast<const float2 *>(envelopes), k, reinterpret_cast<float2 *>(out),
+            oow_total, tx0, (int)tiles, split, part);
+        if (split > 1) {
+            add_parts_kernel<<<4 * sm_count(), 256, 0, s>>>(reinterpret_cast<float2 *>(out), part,
+                                                            split - 1, nv);
+            cudaFreeAsync(part, s);
+        }
+        return check_launch("bpa_tile_kernel");
+    }
+    const int64_t tiles = (int64_t)((nx + CART_V - 1) / CART_V) * ((ny + CART_TY - 1) / CART_TY) *
+                          ((nz + CART_TZ - 1) / CART_TZ);
     bpa_cartesian_kernel<<<(unsigned)tiles, BP_THREADS, 0, s>>>(
         origin[0], origin[1], origin[2], step[0], step[1], step[2], nx, ny, nz, vox_begin,
         vox_end, reinterpret_cast<const float4 *>(el_xyz), (int)m,
