@@ -1,0 +1,157 @@
+"""CPU-only tests: the C-ABI library loads and exports every declared symbol,
+the host-side schedule/geometry logic, workloads, and the error contract.
+No kernel is launched here."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2506_23568_b200 import _native, ffbp, model, workloads
+from paper_2506_23568_b200.dist import chunk_size, shard_range
+from paper_2506_23568_b200.errors import ConfigError
+
+REPO = Path(__file__).resolve().parents[1]
+
+
+def _header_symbols():
+    text = (REPO / "include" / "hhsar_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(hhsar_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.library(require_gpu=False)
+    declared = _header_symbols()
+    assert len(declared) >= 18
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_native.SIGNATURES), "binding and header disagree"
+
+
+def test_struct_layout_matches_library():
+    lib = _native.library(require_gpu=False)
+    out = np.zeros(16, dtype=np.int64)
+    n = lib.hhsar_abi_layout(out.ctypes.data, 16)
+    assert n == 9
+    assert out[0] == _native.GEOM_DTYPE.itemsize
+    assert out[1] == _native.GRID_DTYPE.itemsize
+
+
+def test_library_is_sm100a():
+    import subprocess
+    res = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)], capture_output=True,
+                         text=True)
+    assert "sm_100a" in res.stdout
+
+
+def test_leaf_bounds_match_reference_partition():
+    # model.py:377-382: first n mod L leaves get one extra element
+    b = model.leaf_bounds(4000 * 8, 9)
+    sizes = np.diff(b)
+    assert sizes.size == 256 and sizes.sum() == 32000 and set(sizes) == {125}
+    b = model.leaf_bounds(81, 3)
+    assert list(np.diff(b)) == [21, 20, 20, 20]
+    with pytest.raises(ConfigError):
+        model.leaf_bounds(3, 4)
+
+
+@pytest.mark.parametrize("levels,factor", [(3, 2), (7, 2), (7, 4), (6, 4), (12, 4), (11, 2)])
+def test_schedule_levels_and_fanouts(levels, factor):
+    n = 2 ** (levels - 1) * 3 + 5
+    s = ffbp.Schedule(n, levels, factor)
+    step = int(np.log2(factor))
+    assert s.grid_levels == list(range(1, levels, step))
+    for (a, b), lev in zip(s.level_slices, s.grid_levels):
+        assert b - a == 2 ** (levels - lev)
+        g = s.grids[a:b]
+        assert g["start"][0] == 0 and g["stop"][-1] == n
+        assert np.all(g["start"][1:] == g["stop"][:-1])
+    for k, fan in enumerate(s.fanouts):
+        (a0, a1), (b0, b1) = s.level_slices[k], s.level_slices[k + 1]
+        assert (a1 - a0) == (b1 - b0) * fan
+    assert s.final_children == s.level_slices[-1][1] - s.level_slices[-1][0]
+    assert np.all(s.grids["is_leaf"][:s.level_slices[0][1]] == 1)
+
+
+def test_schedule_rejects_bad_factor():
+    with pytest.raises(ConfigError):
+        ffbp.Schedule(100, 4, 3)
+
+
+def test_geom_constants_bit_identical_to_reference_formulas():
+    w = workloads.config(0)
+    g = ffbp.make_geom(w.region, w.freqs, 1.4, 0.25, 4, 1e-8)[0]
+    k_min, k_max = w.freqs.k_min, w.freqs.k_max
+    assert g["c_uv"] == k_max / np.pi
+    assert g["c_nhi"] == k_max / (2.0 * (2.0 * np.pi))
+    assert g["c_nlo"] == k_min / (2.0 * (2.0 * np.pi))
+    assert g["step"] == 1.0 / 1.4
+    assert g["max_step"] == 0.5 * w.region.diagonal
+
+
+def test_params_validation_matches_reference():
+    with pytest.raises(ConfigError):
+        ffbp.FfbpParams(levels=0)
+    with pytest.raises(ConfigError):
+        ffbp.FfbpParams(gamma=0.9)
+    with pytest.raises(ConfigError):
+        ffbp.FfbpParams(kernel="nearest")
+    with pytest.raises(ConfigError):
+        ffbp.FfbpParams(margin=1.5)
+
+
+def test_default_levels():
+    ap = model.SyntheticAperture(np.zeros((33 * 33, 3)), 33, 33)
+    assert ffbp.default_levels(ap) == 3
+    ap = model.SyntheticAperture(np.zeros((8 * 4000, 3)), 8, 4000)
+    assert ffbp.default_levels(ap) == 1
+
+
+@pytest.mark.parametrize("n,world", [(10, 3), (2560000, 8), (7, 8), (1, 1)])
+def test_shard_ranges_tile_exactly(n, world):
+    ranges = [shard_range(n, r, world) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    for (a, b), (c, d) in zip(ranges[:-1], ranges[1:]):
+        assert b == c
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1 and max(sizes) <= chunk_size(n, world)
+
+
+def test_workloads_match_baseline_shapes():
+    w0 = workloads.config(0)
+    assert w0.n_elements == 1024 and w0.freqs.count == 64 and w0.dims == (64, 64, 32)
+    assert w0.upsample * w0.freqs.count == 512
+    # Morton 4x4 blocks: every contiguous run of 16 elements is one 4x4 block
+    el = np.asarray(w0.aperture.elements)
+    for b in range(0, 1024, 16):
+        blk = el[b:b + 16, :2]
+        assert np.ptp(blk[:, 0]) < 0.0135 and np.ptp(blk[:, 1]) < 0.0135
+    w1 = workloads.config(1)
+    assert w1.n_elements == 32000 and w1.freqs.count == 256 and w1.dims == (200, 200, 64)
+    assert w1.upsample * w1.freqs.count == 1024
+    assert w1.bpa_units == 200 * 200 * 64 * 32000
+    w3 = workloads.config(3, frames=64)
+    assert w3.n_elements == 512 and w3.freqs.count == 512
+    # seeded: identical on regeneration
+    assert np.array_equal(workloads.config(1).aperture.elements, w1.aperture.elements)
+
+
+def test_validate_geometry_contract():
+    ap = model.SyntheticAperture(np.array([[0.0, 0.0, 0.01]]), 1, 1)
+    with pytest.raises(ConfigError):
+        model.validate_geometry(ap, model.ImagingRegion(-1, 1, -1, 1, 0.005, 1))
+    model.validate_geometry(ap, model.ImagingRegion(-1, 1, -1, 1, 0.02, 1))
+
+
+def test_product_path_fails_loudly_without_gpu(monkeypatch):
+    """No CPU fallback: on a GPU-less host the first product call raises."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2506_23568_b200 import NativeUnavailableError, bpa_reconstruct
+    w = workloads.config(0)
+    cube = model.DataCube(np.zeros((w.n_elements, w.freqs.count), np.complex64), w.aperture,
+                          w.freqs)
+    with pytest.raises(NativeUnavailableError):
+        bpa_reconstruct(cube, w.region, dims=(4, 4, 4))
