@@ -81,16 +81,20 @@ typedef struct hhsar_grid_desc {
     int32_t core_lo[3];  /* index range of the region image (ffbp.py:302-304)  */
     int32_t core_hi[3];
     int32_t is_leaf;     /* apply the level-1 delay-window mask                */
+    int32_t act_lo[2];   /* (u, v) index rectangle of the columns Newton must  */
+    int32_t act_hi[2];   /* run: near band AND reachable |tu|, |tv| (empty if  */
+                         /* lo > hi); every other column is masked outright    */
     int64_t start, stop; /* element slice [start, stop)                        */
     int64_t leaf_lo, leaf_hi; /* leaf index range [leaf_lo, leaf_hi)           */
-    int64_t offset;      /* first lattice point in the level pools             */
-    int64_t col_offset;  /* first (u, v) column in the Newton work list        */
+    int64_t offset;      /* first lattice point in the global pools            */
+    int64_t col_offset;  /* first active column in the Newton work list        */
 } hhsar_grid_desc;
 
 /* Per-grid counters written by hhsar_grid_newton (int64 each):
  * [0] valid points, [1] valid core points   (SubimageGrid built, ffbp.py:305)
  * [2] valid after the leaf delay mask, [3] core valid after it (ffbp.py:331-335)
- * [4] Newton iterations executed, [5] domain errors (rad <= gap*1e-12)       */
+ * [4] Newton iterations executed, [5] Newton solves executed (points whose
+ * inversion had to run; pruned columns run none)                             */
 #define HHSAR_GRID_STATS 6
 
 const char *hhsar_last_error(void);
@@ -164,15 +168,18 @@ int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_
                     const double *boundary, int64_t n_b, const hhsar_geom *geom,
                     int32_t *status, void *stream);
 
-/* Newton inversion of every near-band (u, v) column of every grid, warm
+/* Newton inversion of every ACTIVE (u, v) column of every grid (desc.act_*
+ * rectangle, at desc.col_offset in a work list of n_cols columns), warm
  * started along n (ffbp.py:271-282), then the containment, near-band and
  * (leaf grids) delay-window masks.  positions float64 [P][3], valid uint8
- * [P] (P = sum of lattice sizes, at desc.offset), stats int64
- * [n_grids][HHSAR_GRID_STATS] (zeroed by the caller).  n_cols = total
- * columns (sum nu*nv, at desc.col_offset). */
+ * [P] (P = sum of lattice sizes, at desc.offset; the caller zeroes valid,
+ * inactive columns are never touched), stats int64
+ * [n_grids][HHSAR_GRID_STATS] (zeroed by the caller).  block_grid int32
+ * [ceil(n_cols / 128)]: the grid of each 128-column block's first column
+ * (host-built from col_offset; device pointer). */
 int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_cols,
-                      const hhsar_geom *geom, double *positions, uint8_t *valid,
-                      int64_t *stats, void *stream);
+                      const int32_t *block_grid, const hhsar_geom *geom, double *positions,
+                      uint8_t *valid, int64_t *stats, void *stream);
 
 /* ---- HHFFBPA: leaf BPA and merges ----------------------------------------- */
 

@@ -32,7 +32,7 @@ GRID_DTYPE = np.dtype([
     ("origin", "<f8", 3), ("slack_lo", "<f8", 3), ("slack_hi", "<f8", 3),
     ("dims", "<i4", 3), ("near_lo", "<i4", 3), ("near_hi", "<i4", 3),
     ("core_lo", "<i4", 3), ("core_hi", "<i4", 3), ("is_leaf", "<i4"),
-    ("start", "<i8"), ("stop", "<i8"), ("leaf_lo", "<i8"), ("leaf_hi", "<i8"),
+    ("act_lo", "<i4", 2), ("act_hi", "<i4", 2), ("start", "<i8"), ("stop", "<i8"), ("leaf_lo", "<i8"), ("leaf_hi", "<i8"),
     ("offset", "<i8"), ("col_offset", "<i8")], align=True)
 
 GRID_STATS = 6
@@ -56,7 +56,7 @@ SIGNATURES = {
     "hhsar_range_demod": ([_P, _I64, _I64, _D, _D, _F, _P], ctypes.c_int),
     "hhsar_leaf_boxes": ([_P, _P, _I64, _P, _P], ctypes.c_int),
     "hhsar_grid_plan": ([_P, _I64, _P, _P, _I64, _P, _P, _P], ctypes.c_int),
-    "hhsar_grid_newton": ([_P, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "hhsar_grid_newton": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "hhsar_leaf_bp": ([_P, _I64, _P, _P, _P, _P, _I64, _D, _D, _D, _P, _I32, _P, _P, _P],
                       ctypes.c_int),
     "hhsar_merge_level": ([_P, _I64, _I64, _P, _P, _P, _I64, _I32, _P, _P, _I32, _I32, _P, _P,

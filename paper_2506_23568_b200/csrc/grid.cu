@@ -25,71 +25,93 @@ struct NewtonGeom {
     double gap, c_uv, c_nhi, c_nlo;
 };
 
-__device__ __forceinline__ bool newton_solve(const NewtonGeom &G, double tu, double tv, double tn,
-                                             double &x, double &y, double &z, double tol,
-                                             int max_iter, double max_step, double z_floor,
-                                             int &iters) {
-    const double xmn = G.ext[0], xmx = G.ext[1], ymn = G.ext[2], ymx = G.ext[3];
-    bool good = false;
-    int it;
-    for (it = 1; it <= max_iter; ++it) {
-        const double x0 = fmin(fmax(x, xmn), xmx);
-        const double y0 = fmin(fmax(y, ymn), ymx);
-        const double z2 = z * z;
-        const double ax = x - xmn, bx = x - xmx, ay = y - ymn, by = y - ymx;
-        const double yy = (y - y0) * (y - y0), xx = (x - x0) * (x - x0);
-        const double du1 = sqrt(ax * ax + yy + z2), du2 = sqrt(bx * bx + yy + z2);
-        const double dv1 = sqrt(xx + ay * ay + z2), dv2 = sqrt(xx + by * by + z2);
-        const double e1 = sqrt(ax * ax + ay * ay + z2), e2 = sqrt(ax * ax + by * by + z2);
-        const double e3 = sqrt(bx * bx + ay * ay + z2), e4 = sqrt(bx * bx + by * by + z2);
-        const double r = e1 + e2 + e3 + e4;
-        const double rad = r * r - G.gap;
-        if (rad <= 0.0 || fmin(fmin(du1, du2), fmin(dv1, dv2)) == 0.0 ||
-            fmin(fmin(e1, e2), fmin(e3, e4)) == 0.0)
-            break;
-        const double sq = sqrt(rad);
-        const double ru = G.c_uv * (du1 - du2) - tu;
-        const double rv = G.c_uv * (dv1 - dv2) - tv;
-        const double rn = G.c_nhi * sq - G.c_nlo * r - tn;
-        if (fmax(fabs(ru), fmax(fabs(rv), fabs(rn))) <= tol) {
-            good = true;
-            break;
-        }
-        const double i1 = 1.0 / du1, i2 = 1.0 / du2, i3 = 1.0 / dv1, i4 = 1.0 / dv2;
-        const double ja = G.c_uv * (ax * i1 - bx * i2);
-        const double jb = G.c_uv * ((y - y0) * i1 - (y - y0) * i2);
-        const double jc = G.c_uv * (z * i1 - z * i2);
-        const double jd = G.c_uv * ((x - x0) * i3 - (x - x0) * i4);
-        const double je = G.c_uv * (ay * i3 - by * i4);
-        const double jf = G.c_uv * (z * i3 - z * i4);
-        const double fac = G.c_nhi * (r / sq) - G.c_nlo;
-        const double f1 = 1.0 / e1, f2 = 1.0 / e2, f3 = 1.0 / e3, f4 = 1.0 / e4;
-        const double jg = fac * (ax * f1 + ax * f2 + bx * f3 + bx * f4);
-        const double jh = fac * (ay * f1 + by * f2 + ay * f3 + by * f4);
-        const double ji = fac * (z * (f1 + f2 + f3 + f4));
-        const double m0 = je * ji - jf * jh, m1 = jd * ji - jf * jg, m2 = jd * jh - je * jg;
-        const double det = ja * m0 - jb * m1 + jc * m2;
-        if (fabs(det) < 1e-30) break;
-        const double idet = 1.0 / det;
-        double sx = (ru * m0 - jb * (rv * ji - jf * rn) + jc * (rv * jh - je * rn)) * idet;
-        double sy = (ja * (rv * ji - jf * rn) - ru * m1 + jc * (jd * rn - rv * jg)) * idet;
-        double sz = (ja * (je * rn - rv * jh) - jb * (jd * rn - rv * jg) + ru * m2) * idet;
-        if (max_step > 0.0) {
-            const double sn = sqrt(sx * sx + sy * sy + sz * sz);
-            if (sn > max_step) {
-                const double sc = max_step / sn;
-                sx *= sc;
-                sy *= sc;
-                sz *= sc;
-            }
-        }
-        x -= sx;
-        y -= sy;
-        z -= sz;
-        if (z < z_floor) z = z_floor;
+// ---- one Newton iteration, SFU-seeded float64 reciprocal square roots ---------
+// Every distance the iteration needs is d = a * rsqrt(a) with a the squared
+// distance; its reciprocal (Jacobian) is rsqrt(a) itself, so the 8 sqrt + 9
+// divisions of the textbook form become 9 rsqrt + 1 reciprocal.  rsqrt is
+// seeded by the fp32 SFU and refined twice (error 1e-7 -> 1e-14 -> ~1 ulp).
+__device__ __forceinline__ double rsqrt_d(double a) {
+    double y = (double)rsqrtf((float)a);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double e = fma(-(a * y), y, 1.0);
+        y = fma(0.5 * y, e, y);
     }
-    iters = it > max_iter ? max_iter : it;
-    return good;
+    return y;
+}
+
+__device__ __forceinline__ double rcp_d(double a) {
+    double y = (double)__frcp_rn((float)a);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) y = fma(y, fma(-a, y, 1.0), y);
+    return y;
+}
+
+// Returns 1 when the residual at (x, y, z) is within tol (converged), 2 when
+// the reference would give up here (rad <= 0, a zero distance, singular
+// Jacobian), 0 after taking one damped step (same formulas as
+// _kernels.py:277-340).
+__device__ __forceinline__ int newton_iteration(const NewtonGeom &G, double tu, double tv,
+                                                double tn, double &x, double &y, double &z,
+                                                double tol, double max_step2, double max_step,
+                                                double z_floor) {
+    const double xmn = G.ext[0], xmx = G.ext[1], ymn = G.ext[2], ymx = G.ext[3];
+    const double x0 = fmin(fmax(x, xmn), xmx);
+    const double y0 = fmin(fmax(y, ymn), ymx);
+    const double z2 = z * z;
+    const double ax = x - xmn, bx = x - xmx, ay = y - ymn, by = y - ymx;
+    const double yd = y - y0, xd = x - x0;
+    const double yy = yd * yd, xx = xd * xd;
+    const double ax2 = ax * ax, bx2 = bx * bx, ay2 = ay * ay, by2 = by * by;
+    const double a_u1 = ax2 + yy + z2, a_u2 = bx2 + yy + z2;
+    const double a_v1 = xx + ay2 + z2, a_v2 = xx + by2 + z2;
+    const double a_e1 = ax2 + ay2 + z2, a_e2 = ax2 + by2 + z2;
+    const double a_e3 = bx2 + ay2 + z2, a_e4 = bx2 + by2 + z2;
+    if (fmin(fmin(fmin(a_u1, a_u2), fmin(a_v1, a_v2)), fmin(fmin(a_e1, a_e2), fmin(a_e3, a_e4))) ==
+        0.0)
+        return 2;
+    const double i1 = rsqrt_d(a_u1), i2 = rsqrt_d(a_u2), i3 = rsqrt_d(a_v1), i4 = rsqrt_d(a_v2);
+    const double f1 = rsqrt_d(a_e1), f2 = rsqrt_d(a_e2), f3 = rsqrt_d(a_e3), f4 = rsqrt_d(a_e4);
+    const double r = a_e1 * f1 + a_e2 * f2 + a_e3 * f3 + a_e4 * f4;
+    const double rad = r * r - G.gap;
+    if (rad <= 0.0) return 2;
+    const double irad = rsqrt_d(rad);
+    const double sq = rad * irad;
+    const double ru = G.c_uv * (a_u1 * i1 - a_u2 * i2) - tu;
+    const double rv = G.c_uv * (a_v1 * i3 - a_v2 * i4) - tv;
+    const double rn = G.c_nhi * sq - G.c_nlo * r - tn;
+    if (fmax(fabs(ru), fmax(fabs(rv), fabs(rn))) <= tol) return 1;
+    const double ja = G.c_uv * (ax * i1 - bx * i2);
+    const double jb = G.c_uv * (yd * (i1 - i2));
+    const double jc = G.c_uv * (z * (i1 - i2));
+    const double jd = G.c_uv * (xd * (i3 - i4));
+    const double je = G.c_uv * (ay * i3 - by * i4);
+    const double jf = G.c_uv * (z * (i3 - i4));
+    const double fac = G.c_nhi * (r * irad) - G.c_nlo;
+    const double jg = fac * (ax * (f1 + f2) + bx * (f3 + f4));
+    const double jh = fac * (ay * (f1 + f3) + by * (f2 + f4));
+    const double ji = fac * (z * (f1 + f2 + f3 + f4));
+    const double m0 = je * ji - jf * jh, m1 = jd * ji - jf * jg, m2 = jd * jh - je * jg;
+    const double det = ja * m0 - jb * m1 + jc * m2;
+    if (fabs(det) < 1e-30) return 2;
+    const double idet = rcp_d(det);
+    double sx = (ru * m0 - jb * (rv * ji - jf * rn) + jc * (rv * jh - je * rn)) * idet;
+    double sy = (ja * (rv * ji - jf * rn) - ru * m1 + jc * (jd * rn - rv * jg)) * idet;
+    double sz = (ja * (je * rn - rv * jh) - jb * (jd * rn - rv * jg) + ru * m2) * idet;
+    if (max_step > 0.0) {
+        const double sn2 = sx * sx + sy * sy + sz * sz;
+        if (sn2 > max_step2) {
+            const double sc = max_step * rsqrt_d(sn2);
+            sx *= sc;
+            sy *= sc;
+            sz *= sc;
+        }
+    }
+    x -= sx;
+    y -= sy;
+    z -= sz;
+    if (z < z_floor) z = z_floor;
+    return 0;
 }
 
 // ---- leaf boxes ----------------------------------------------------------------
@@ -239,59 +261,83 @@ grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__
         D.hi[a] = hi[a];
         D.box[a] = mn[a];
         D.box[3 + a] = mx[a];
+        if (a < 2) {
+            // Active columns: the near band intersected with the reachable
+            // targets.  |u| < (k_max/pi) dx for every point with z > 0
+            // (triangle inequality on du1 - du2; v likewise), so a column with
+            // |tu| >= (k_max/pi) dx + 2 tol cannot converge on any plane: all
+            // its points fail -- which also keeps its warm-start chain at the
+            // region centre -- and are masked without running Newton.  These
+            // are the u/v planes the reference keeps just beyond the limit
+            // (ffbp.py:248-257).  Both sets are index intervals.
+            const double lim = g.c_uv * (ext[2 * a + 1] - ext[2 * a]) + 2.0 * g.tol;
+            int a0 = -1, a1 = -2;
+            for (int i = n0; i <= n1; ++i) {
+                const double t = xadd(origin[a], xmul(step, (double)i));
+                if (fabs(t) < lim) {
+                    if (a0 < 0) a0 = i;
+                    a1 = i;
+                }
+            }
+            if (a0 < 0) a0 = 0;
+            D.act_lo[a] = a0;
+            D.act_hi[a] = a1;
+        }
     }
     for (int k = 0; k < 4; ++k) D.ext[k] = ext[k];
 }
 
 // ---- Newton columns -------------------------------------------------------------
-__device__ __forceinline__ int find_grid(const hhsar_grid_desc *__restrict__ grids, int n,
-                                         int64_t key, bool by_col) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {  // last grid whose start <= key
-        const int mid = (lo + hi + 1) >> 1;
-        const int64_t s = by_col ? grids[mid].col_offset : grids[mid].offset;
-        if (s <= key) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
 __global__ void __launch_bounds__(128)
 grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
-                   hhsar_geom g, double *__restrict__ positions, uint8_t *__restrict__ valid,
+                   const int32_t *__restrict__ block_grid, hhsar_geom g,
+                   double *__restrict__ positions, uint8_t *__restrict__ valid,
                    int64_t *__restrict__ stats) {
+    // Work list = the active columns only (desc.act_* rectangle, see
+    // grid_plan_kernel): columns outside the near band are masked whatever
+    // Newton returns (ffbp.py:294-301) and unreachable ones provably fail,
+    // so neither is launched (the caller zeroed `valid`).
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_cols) return;
-    const int gi = find_grid(grids, n_grids, c, true);
+    int gi = block_grid[blockIdx.x];
+    while (gi + 1 < n_grids && grids[gi + 1].col_offset <= c) ++gi;
     const hhsar_grid_desc &D = grids[gi];
-    const int nu = D.dims[0], nv = D.dims[1], nn = D.dims[2];
-    const int64_t col = c - D.col_offset;
-    const int iu = (int)(col / nv), iv = (int)(col % nv);
+    const int nv = D.dims[1], nn = D.dims[2];
+    const int64_t k = c - D.col_offset;
+    const int wv = D.act_hi[1] - D.act_lo[1] + 1;
+    const int iu = D.act_lo[0] + (int)(k / wv), iv = D.act_lo[1] + (int)(k % wv);
+    const int64_t col = (int64_t)iu * nv + iv;
     uint8_t *vcol = valid + D.offset + col * nn;
     double *pcol = positions + 3 * (D.offset + col * nn);
-    (void)nu;
-    unsigned n_pre = 0, core_pre = 0, n_post = 0, core_post = 0, its = 0;
-    const bool near_col = iu >= D.near_lo[0] && iu <= D.near_hi[0] && iv >= D.near_lo[1] &&
-                          iv <= D.near_hi[1];
-    const int w_end = near_col ? D.near_hi[2] + 1 : 0;
-    if (near_col && w_end > 0) {
+    unsigned n_pre = 0, core_pre = 0, n_post = 0, core_post = 0, its = 0, solves = 0;
+    const double tu = xadd(D.origin[0], xmul(g.step, (double)iu));
+    const double tv = xadd(D.origin[1], xmul(g.step, (double)iv));
+    const int w_end = D.near_hi[2] + 1;
+    if (w_end > 0) {
         NewtonGeom G;
         for (int k = 0; k < 4; ++k) G.ext[k] = D.ext[k];
         G.gap = box_gap_exact(D.ext);
         G.c_uv = g.c_uv;
         G.c_nhi = g.c_nhi;
         G.c_nlo = g.c_nlo;
-        const double tu = xadd(D.origin[0], xmul(g.step, (double)iu));
-        const double tv = xadd(D.origin[1], xmul(g.step, (double)iv));
         const bool core_uv = iu >= D.core_lo[0] && iu <= D.core_hi[0] && iv >= D.core_lo[1] &&
                              iv <= D.core_hi[1];
+        // Flattened march: every lane runs its own (plane, iteration) state, so
+        // a warp costs max over lanes of the TOTAL iterations instead of the
+        // sum over planes of the per-plane maximum.
+        const double max_step2 = g.max_step * g.max_step;
         double gx = g.center[0], gy = g.center[1], gz = g.center[2];
-        for (int w = 0; w < w_end; ++w) {
-            const double tn = xadd(D.origin[2], xmul(g.step, (double)w));
-            double x = gx, y = gy, z = gz > g.z_floor ? gz : g.z_floor;
-            int it = 0;
-            const bool ok = newton_solve(G, tu, tv, tn, x, y, z, g.tol, g.max_iter, g.max_step,
-                                         g.z_floor, it);
+        int w = 0, it = 0;
+        double tn = D.origin[2];
+        double x = gx, y = gy, z = gz > g.z_floor ? gz : g.z_floor;
+        while (w < w_end) {
+            ++it;
+            int st = newton_iteration(G, tu, tv, tn, x, y, z, g.tol, max_step2, g.max_step,
+                                      g.z_floor);
+            if (st == 0 && it < g.max_iter) continue;
+            const bool ok = st == 1;
             its += it;
+            ++solves;
             uint8_t v = 0;
             if (w >= D.near_lo[2]) {
                 bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] && y >= D.slack_lo[1] &&
@@ -333,6 +379,12 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                 gy = g.center[1];
                 gz = g.center[2];
             }
+            ++w;
+            it = 0;
+            tn = xadd(D.origin[2], xmul(g.step, (double)w));
+            x = gx;
+            y = gy;
+            z = gz > g.z_floor ? gz : g.z_floor;
         }
     }
     for (int w = w_end; w < nn; ++w) vcol[w] = 0;
@@ -342,6 +394,7 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
     if (n_post) atomicAdd((unsigned long long *)(st + 2), (unsigned long long)n_post);
     if (core_post) atomicAdd((unsigned long long *)(st + 3), (unsigned long long)core_post);
     if (its) atomicAdd((unsigned long long *)(st + 4), (unsigned long long)its);
+    if (solves) atomicAdd((unsigned long long *)(st + 5), (unsigned long long)solves);
 }
 
 __global__ void invert_newton_kernel(NewtonGeom G, const double *__restrict__ t,
@@ -353,9 +406,13 @@ __global__ void invert_newton_kernel(NewtonGeom G, const double *__restrict__ t,
     if (i >= n) return;
     const double gz = gs[3 * i + 2] > z_floor ? gs[3 * i + 2] : z_floor;
     double x = gs[3 * i], y = gs[3 * i + 1], z = gz;
-    int it = 0;
-    const bool good = newton_solve(G, t[3 * i], t[3 * i + 1], t[3 * i + 2], x, y, z, tol, max_iter,
-                                   max_step, z_floor, it);
+    int it = 0, st = 0;
+    while (st == 0 && it < max_iter) {
+        ++it;
+        st = newton_iteration(G, t[3 * i], t[3 * i + 1], t[3 * i + 2], x, y, z, tol,
+                              max_step * max_step, max_step, z_floor);
+    }
+    const bool good = st == 1;
     iters[i] = it;
     ok[i] = good;
     pos[3 * i] = good ? x : gs[3 * i];
@@ -386,12 +443,14 @@ extern "C" int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const do
 }
 
 extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_cols,
-                                 const hhsar_geom *geom, double *positions, uint8_t *valid,
-                                 int64_t *stats, void *stream) {
+                                 const int32_t *block_grid, const hhsar_geom *geom,
+                                 double *positions, uint8_t *valid, int64_t *stats,
+                                 void *stream) {
     HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
+    HHSAR_REQUIRE(n_cols == 0 || block_grid != nullptr, "grid_newton: block_grid required");
     if (n_cols == 0) return HHSAR_OK;
     grid_newton_kernel<<<(unsigned)((n_cols + 127) / 128), 128, 0, as_stream(stream)>>>(
-        grids, (int)n_grids, n_cols, *geom, positions, valid, stats);
+        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats);
     return check_launch("grid_newton_kernel");
 }
 

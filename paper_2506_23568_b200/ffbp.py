@@ -197,15 +197,21 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     dims = host["dims"].astype(np.int64)
     npts = dims.prod(axis=1)
     host["offset"] = np.concatenate([[0], np.cumsum(npts)[:-1]])
-    cols = dims[:, 0] * dims[:, 1]
-    host["col_offset"] = np.concatenate([[0], np.cumsum(cols)[:-1]])
+    # Newton work list: the active (u, v) rectangle of every grid
+    span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
+    cols = span[:, 0] * span[:, 1]
+    starts = np.concatenate([[0], np.cumsum(cols)[:-1]])
+    host["col_offset"] = starts
+    n_cols = int(cols.sum())
+    block_grid = np.searchsorted(starts, np.arange(0, max(n_cols, 1), 128), side="right") - 1
     descs_dev.copy_(torch.from_numpy(host.view(np.uint8).reshape(-1)), non_blocking=False)
     total = int(npts.sum())
     positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
-    valid = torch.empty(total, dtype=torch.uint8, device=dev)
+    valid = torch.zeros(total, dtype=torch.uint8, device=dev)
     stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
-    _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, int(cols.sum()),
-                 _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
+    bg = torch.as_tensor(block_grid.astype(np.int32), device=dev)
+    _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, n_cols,
+                 _native.ptr(bg), _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
                  _native.ptr(stats), stream)
     return Lattices(host, descs_dev, positions, valid, stats, geom)
 

@@ -1,0 +1,96 @@
+"""Per-stage device timing of the HHFFBPA pipeline (CUDA events) for a
+BASELINE config, plus optional parity against the CPU oracle."""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--levels", type=int, default=None)
+    ap.add_argument("--factor", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--oracle", action="store_true")
+    args = ap.parse_args()
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, ffbp, rangecomp, workloads
+    w = workloads.config(args.config, frames=args.frames)
+    levels = args.levels or w.levels
+    factor = args.factor or w.merge_factor
+    t = time.perf_counter()
+    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                            w.freqs.k_samples)
+    torch.cuda.synchronize()
+    t_sim = time.perf_counter() - t
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    el4 = bpa.el_f32x4(el)
+    params = ffbp.FfbpParams(levels=levels)
+    ev = {}
+
+    orig_call = _native.call
+
+    def timed_call(name, *a):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        orig_call(name, *a)
+        e.record()
+        ev.setdefault(name, []).append((s, e))
+
+    res = []
+    for rep in range(args.reps + 1):
+        ev.clear()
+        _native.call = timed_call
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
+        run = ffbp.hhffbpa_device(env, el, el4, 0.0, dt, k_ref, w.freqs, w.region, w.dims,
+                                  params, levels, factor)
+        t1.record()
+        torch.cuda.synchronize()
+        _native.call = orig_call
+        stages = {k: round(sum(s.elapsed_time(e) for s, e in v), 3) for k, v in ev.items()}
+        res.append({"total_ms": round(t0.elapsed_time(t1), 3), "stages_ms": stages})
+    stats = run.lattices.stats.cpu().numpy()
+    flags = run.flags.cpu().numpy()
+    out = {"config": args.config, "levels": levels, "merge_factor": factor,
+           "n_elements": w.n_elements, "dims": list(w.dims), "n_grids": int(run.sched.n_grids),
+           "lattice_points": int(run.lattices.npts.sum()),
+           "valid_points": int(stats[:, 0].sum()),
+           "newton_iterations": int(stats[:, 4].sum()),
+           "leaf_units": int(sum(stats[g, 2] * (run.lattices.descs['stop'][g] - run.lattices.descs['start'][g])
+                                for g in range(*run.sched.level_slices[0]))),
+           "flags": flags.tolist(), "sim_s": round(t_sim, 2), "runs": res[1:]}
+    best = min(r["total_ms"] for r in res[1:])
+    out["best_ms"] = best
+    out["bpa_equiv_gunits_per_s"] = round(w.n_voxels * w.n_elements / (best / 1e3) / 1e9, 1)
+    out["volumes_per_s"] = round(1e3 / best, 2)
+    if args.oracle:
+        import oracle
+        from paper_2506_23568_b200.model import DataCube
+        host = DataCube(values=cube.cpu().numpy(), aperture=w.aperture, freqs=w.freqs)
+        t = time.perf_counter()
+        want, _, _, prov = oracle.hhffbpa_reconstruct(host, w.region, w.dims, levels=levels,
+                                                      upsample=w.upsample, merge_factor=factor)
+        out["oracle_s"] = round(time.perf_counter() - t, 2)
+        got = run.volume.cpu().numpy().reshape(w.dims)
+        out["rel_l2_vs_oracle"] = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+        out["peak_equal"] = bool(np.argmax(np.abs(got)) == np.argmax(np.abs(want)))
+        lp = [[int(v) for v in stats[a:b, 2 if k == 0 else 0]]
+              for k, (a, b) in enumerate(run.sched.level_slices)]
+        out["level_points_equal"] = lp == prov["level_points"][:-1]
+        out["oracle_flags"] = prov["merge_flags"] + [prov["final_flags"]]
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
