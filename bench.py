@@ -233,12 +233,21 @@ def run_ours(args):
         achieved = shard_units / (kms / 1e3) / 1e9
         peak = sfu_peak_units(sms, max_mhz) / 1e9
         hbm_bytes = n_el * n_t * 8 + (ve - vb) * 8
+        traffic = None
+        try:
+            t = json.loads((REPO / "profiles" / "traffic.json").read_text())["bpa_tile_kernel"]
+            traffic = int(t["dram_read_bytes"] + t["dram_write_bytes"])
+        except Exception:
+            pass
         roofline = {
-            "kernel": "bpa_cartesian_kernel", "bound": "sfu", "achieved": round(achieved, 2),
+            "kernel": "bpa_tile_kernel (hhsar_bpa_cartesian)", "bound": "sfu",
+            "achieved": round(achieved, 2),
             "peak": round(peak, 2), "unit": "Gunit/s", "frac": round(achieved / peak, 4),
             "peak_source": f"{sms} SMs x 16 MUFU/clk x {max_mhz:.0f} MHz / 3 MUFU per unit "
                            "(rsqrt, sin, cos); MEASURED_PEAKS.json has no SFU figure",
-            "traffic": None, "kernel_ms": round(kms, 3),
+            "traffic": traffic,
+            "traffic_source": "profiles/traffic.json (ncu --set full, DRAM read+write per launch)",
+            "kernel_ms": round(kms, 3),
             "share_of_step": round(kms / ms, 4),
             "hbm": {"achieved_gbs": round(hbm_bytes / (kms / 1e3) / 1e9, 1),
                     "peak_gbs": peaks.get("hbm_gbs", 6542.1),
