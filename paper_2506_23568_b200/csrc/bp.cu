@@ -60,7 +60,7 @@ __device__ __forceinline__ bool bp_unit(float d, const BpConst &k, const float2 
 // round-to-integer trick on the FMA pipe (no F2I/I2F/FRND), sqrt is the SFU
 // approximation, and sin/cos take an explicitly range-reduced argument.
 // ---------------------------------------------------------------------------
-constexpr int TL_VX = 4, TL_TY = 16, TL_TZ = 16;  // 4 x 16 x 16 = 1024 voxels
+constexpr int TL_TY = 16, TL_TZ = 16;  // VX x 16 x 16 voxels per tile (VX: template)
 constexpr int TL_THREADS = TL_TY * TL_TZ;
 constexpr int TL_CHUNK = 64;   // elements per staging pass
 constexpr int TL_W = 32;       // staged bins per element (32 x 16 B = 512 B)
@@ -69,9 +69,12 @@ constexpr unsigned MAGIC_BITS = 0x4B400000u;
 
 struct BpFast {
     float inv_bin, x0, rev, xmax;
-    float cbin;   // -0.5 - x0
-    float kfrac;  // MAGIC - x0
+    float cbin;    // -0.5 - x0
+    float kfrac;   // MAGIC - x0
+    float alpha;   // k_ref c dt: carrier radians per delay bin
     int n_t;
+    double alpha_d;  // the same in float64 (staging)
+    double kc_t0;    // k_ref c t0
 };
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -80,12 +83,20 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
-__global__ void __launch_bounds__(TL_THREADS)
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <int VX, int MINB, bool PAIR>
+__global__ void __launch_bounds__(TL_THREADS, MINB)
 bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx, int ny,
                 int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el, int m,
                 const float2 *__restrict__ env, BpFast k, float2 *__restrict__ out,
                 int64_t *__restrict__ oow_total, int tx_base, int n_tiles, int split,
                 float2 *__restrict__ part) {
+    constexpr int TL_VX = VX;  // voxels per thread along x
     __shared__ float4 s_env[TL_CHUNK * TL_W];  // 32 KB
     __shared__ float4 s_el[TL_CHUNK];          // x, y, z, bits(byte offset | -1 = slow)
     __shared__ int s_lo[TL_CHUNK];
@@ -105,15 +116,16 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
     const float py = (float)__dadd_rn(oy, __dmul_rn(sy, (double)iyc));
     const float pz = (float)__dadd_rn(oz, __dmul_rn(sz, (double)izc));
     float px[TL_VX];
-    bool live[TL_VX];
-    int64_t flat[TL_VX];
 #pragma unroll
-    for (int v = 0; v < TL_VX; ++v) {
-        const int ix = ix0 + v;
-        px[v] = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix, nx - 1)));
-        flat[v] = ((int64_t)ix * ny + iy) * nz + iz;
-        live[v] = ix < nx && iy < ny && iz < nz && flat[v] >= vb && flat[v] < ve;
-    }
+    for (int v = 0; v < TL_VX; ++v)
+        px[v] = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix0 + v, nx - 1)));
+    // flattened index / ownership of voxel v, recomputed where needed (keeps
+    // the inner loop's register budget for the accumulators)
+    auto flat_of = [&](int v) { return ((int64_t)(ix0 + v) * ny + iy) * nz + iz; };
+    auto live_of = [&](int v) {
+        const int64_t f = flat_of(v);
+        return ix0 + v < nx && iy < ny && iz < nz && f >= vb && f < ve;
+    };
     // tile bounding box (float32, from the clamped corner voxels)
     const float bx0 = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix0, nx - 1)));
     const float bx1 = (float)__dadd_rn(ox, __dmul_rn(sx, (double)min(ix0 + TL_VX - 1, nx - 1)));
@@ -122,9 +134,13 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
     const float bz0 = (float)__dadd_rn(oz, __dmul_rn(sz, (double)min(tz * TL_TZ, nz - 1)));
     const float bz1 = (float)__dadd_rn(oz, __dmul_rn(sz, (double)min(tz * TL_TZ + TL_TZ - 1, nz - 1)));
 
-    float2 acc[TL_VX];
+    static_assert(!PAIR || VX % 2 == 0, "pair path needs an even VX");
+    float2 acc[PAIR ? 1 : TL_VX];
+    f2x pa[PAIR ? TL_VX : 1], pb[PAIR ? TL_VX : 1];
 #pragma unroll
-    for (int v = 0; v < TL_VX; ++v) acc[v] = make_float2(0.f, 0.f);
+    for (int v = 0; v < (PAIR ? TL_VX : 1); ++v) pa[v] = pb[v] = pk2(0.f, 0.f);
+#pragma unroll
+    for (int v = 0; v < (PAIR ? 1 : TL_VX); ++v) acc[v] = make_float2(0.f, 0.f);
     unsigned bad = 0;
     const BpConst kc{k.inv_bin, k.x0, k.rev, k.xmax, k.n_t};
 
@@ -156,8 +172,12 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
             const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
             const float2 v0 = __ldg(row + min(bin, k.n_t - 1));
             const float2 v1 = __ldg(row + min(bin + 1, k.n_t - 1));
-            s_env[q] = bin < k.n_t - 1 ? make_float4(v0.x, v0.y, v1.x - v0.x, v1.y - v0.y)
-                                       : make_float4(v0.x, v0.y, 0.f, 0.f);
+            // pre-rotate by the carrier at the bin: k_ref c (t0 + bin dt), float64
+            const float2 r = cis_reduced(k.kc_t0 + k.alpha_d * (double)bin);
+            const float2 dv = bin < k.n_t - 1 ? make_float2(v1.x - v0.x, v1.y - v0.y)
+                                              : make_float2(0.f, 0.f);
+            const float2 a = cmul(v0, r), b2 = cmul(dv, r);
+            s_env[q] = make_float4(a.x, a.y, b2.x, b2.y);
         }
         __syncthreads();
         for (int j = 0; j < cn; ++j) {
@@ -165,27 +185,65 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
             const float dy = py - e.y, dz = pz - e.z;
             const float dyz = fmaf(dy, dy, dz * dz);
             const int offb = __float_as_int(e.w);
-            if (offb != -1) {
+            // one fast unit at distance d: window lookup + lerp + carrier + MAC
+            auto unit = [&](float d, unsigned base, float2 &a) {
+                // i = round(x - 0.5) = floor(x) (x - 1 at exact integers, f = 1):
+                // MAGIC + (x - 0.5) rounds at the units place.  (MAGIC - 0.5 is
+                // not an fp32 number, so the 0.5 shift cannot ride in one FFMA.)
+                const float tb = __fadd_rn(fmaf(d, k.inv_bin, k.cbin), MAGIC);
+                // f = x - i = d * inv_bin + (MAGIC - x0 - tb): one rounding
+                const float f = fmaf(d, k.inv_bin, __fsub_rn(k.kfrac, tb));
+                const unsigned byte = (unsigned)__float_as_int(tb) * 16u + base;
+                const float4 w = *reinterpret_cast<const float4 *>(
+                    reinterpret_cast<const char *>(s_env) + byte);
+                const float er = fmaf(f, w.z, w.x), ei = fmaf(f, w.w, w.y);
+                // The carrier k_ref c tau = alpha (x + x0) splits into the
+                // staged bin rotation (alpha (i + x0), exact float64) and
+                // alpha f with f in [0, 1]: the explicit range reduction is
+                // free and the SFU sees |angle| <= alpha (a few revolutions).
+                float s, c;
+                __sincosf(k.alpha * f, &s, &c);
+                a.x = fmaf(er, c, fmaf(-ei, s, a.x));
+                a.y = fmaf(er, s, fmaf(ei, c, a.y));
+            };
+            if (PAIR && offb != -1) {  // compile-time PAIR
+                // Voxels in pairs with packed fp32x2 arithmetic (FADD2/FFMA2/
+                // FMUL2): same per-lane operations and roundings as `unit`,
+                // half the FMA-pipe issue slots.  The complex MAC is kept as two
+                // pair accumulators A += (er, ei) c, B += (er, ei) s, combined
+                // once at the end: re = A.x - B.y, im = A.y + B.x.
+                const unsigned base = (unsigned)offb;
+                const f2x nex = bc2(-e.x), vdyz = bc2(dyz);
+#pragma unroll
+                for (int v = 0; v < TL_VX; v += 2) {
+                    const f2x dx = add2(pk2(px[v], px[v + 1]), nex);
+                    const f2x a2 = fma2(dx, dx, vdyz);
+                    const f2x d = pk2(sqrt_approx(lo2(a2)), sqrt_approx(hi2(a2)));
+                    const f2x tb = add2(fma2(d, bc2(k.inv_bin), bc2(k.cbin)), bc2(MAGIC));
+                    const f2x f = fma2(d, bc2(k.inv_bin), sub2(bc2(k.kfrac), tb));
+                    const unsigned b0 = (unsigned)__float_as_int(lo2(tb)) * 16u + base;
+                    const unsigned b1 = (unsigned)__float_as_int(hi2(tb)) * 16u + base;
+                    const float4 w0 = *reinterpret_cast<const float4 *>(
+                        reinterpret_cast<const char *>(s_env) + b0);
+                    const float4 w1 = *reinterpret_cast<const float4 *>(
+                        reinterpret_cast<const char *>(s_env) + b1);
+                    const f2x e0 = fma2(bc2(lo2(f)), pk2(w0.z, w0.w), pk2(w0.x, w0.y));
+                    const f2x e1 = fma2(bc2(hi2(f)), pk2(w1.z, w1.w), pk2(w1.x, w1.y));
+                    const f2x ang = mul2(f, bc2(k.alpha));
+                    float s0, c0, s1, c1;
+                    __sincosf(lo2(ang), &s0, &c0);
+                    __sincosf(hi2(ang), &s1, &c1);
+                    pa[v] = fma2(e0, bc2(c0), pa[v]);
+                    pb[v] = fma2(e0, bc2(s0), pb[v]);
+                    pa[v + 1] = fma2(e1, bc2(c1), pa[v + 1]);
+                    pb[v + 1] = fma2(e1, bc2(s1), pb[v + 1]);
+                }
+            } else if (offb != -1) {
+                const unsigned base = (unsigned)offb & ~1u;
 #pragma unroll
                 for (int v = 0; v < TL_VX; ++v) {
                     const float dx = px[v] - e.x;
-                    const float d = sqrt_approx(fmaf(dx, dx, dyz));
-                    // i = round(x - 0.5) = floor(x) (x - 1 at exact integers, f = 1):
-                    // MAGIC + (x - 0.5) rounds at the units place.  (MAGIC - 0.5 is
-                    // not an fp32 number, so the 0.5 shift cannot ride in one FFMA.)
-                    const float tb = __fadd_rn(fmaf(d, k.inv_bin, k.cbin), MAGIC);
-                    // f = x - i = d * inv_bin + (MAGIC - x0 - tb): one rounding
-                    const float f = fmaf(d, k.inv_bin, __fsub_rn(k.kfrac, tb));
-                    const unsigned byte = (unsigned)__float_as_int(tb) * 16u + (unsigned)offb;
-                    const float4 w = *reinterpret_cast<const float4 *>(
-                        reinterpret_cast<const char *>(s_env) + byte);
-                    const float er = fmaf(f, w.z, w.x), ei = fmaf(f, w.w, w.y);
-                    const float r1 = fmaf(d, k.rev, MAGIC);              // MAGIC + round(revs)
-                    const float red = fmaf(d, k.rev, -__fsub_rn(r1, MAGIC));  // in [-0.5, 0.5]
-                    float s, c;
-                    __sincosf(6.2831853f * red, &s, &c);
-                    acc[v].x = fmaf(er, c, fmaf(-ei, s, acc[v].x));
-                    acc[v].y = fmaf(er, s, fmaf(ei, c, acc[v].y));
+                    unit(sqrt_approx(fmaf(dx, dx, dyz)), base, acc[v]);
                 }
             } else {
                 const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
@@ -193,10 +251,15 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
                 for (int v = 0; v < TL_VX; ++v) {
                     const float dx = px[v] - e.x;
                     const float d = sqrtf(fmaf(dx, dx, dyz));
-                    float2 a = acc[v];
+                    float2 a = make_float2(0.f, 0.f);
                     const bool ok = bp_unit(d, kc, row, a);
-                    if (live[v]) {
-                        acc[v] = a;
+                    if (live_of(v)) {
+                        if constexpr (PAIR) {
+                            pa[v] = add2(pa[v], pk2(a.x, a.y));  // (re, im) of the term
+                        } else {
+                            acc[v].x += a.x;
+                            acc[v].y += a.y;
+                        }
                         bad += !ok;
                     }
                 }
@@ -205,8 +268,13 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
     }
     float2 *dst = sidx == 0 ? out : part + (int64_t)(sidx - 1) * (ve - vb);
 #pragma unroll
-    for (int v = 0; v < TL_VX; ++v)
-        if (live[v]) dst[flat[v] - vb] = acc[v];
+    for (int v = 0; v < TL_VX; ++v) {
+        if (!live_of(v)) continue;
+        if constexpr (PAIR)
+            dst[flat_of(v) - vb] = make_float2(lo2(pa[v]) - hi2(pb[v]), hi2(pa[v]) + lo2(pb[v]));
+        else
+            dst[flat_of(v) - vb] = acc[v];
+    }
     if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
 }
 
@@ -328,13 +396,8 @@ __global__ void el_to_f32x4(const double *__restrict__ el, int64_t m, float4 *__
 // Element-split factor that best fills the last wave: work items = tiles x
 // split, resident slots = SMs x CTAs/SM; pick split in [1, 8] maximising
 // items / (slots * ceil(items / slots)) (ties -> smaller split).
-int tile_split(int64_t tiles, int64_t m) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpa_tile_kernel, TL_THREADS, 0);
-        if (per_sm <= 0) per_sm = 1;
-    }
-    const double slots = (double)sm_count() * per_sm;
+int tile_split(int64_t tiles, int64_t m, int per_sm) {
+    const double slots = (double)sm_count() * (per_sm > 0 ? per_sm : 1);
     int best = 1;
     double best_eff = 0.0;
     for (int sp = 1; sp <= 8 && (int64_t)sp * TL_CHUNK <= m; ++sp) {
@@ -346,6 +409,49 @@ int tile_split(int64_t tiles, int64_t m) {
         }
     }
     return best;
+}
+
+struct TileArgs {
+    const double *origin, *step;
+    int nx, ny, nz;
+    int64_t vb, ve;
+    const float4 *el;
+    int m;
+    const float2 *env;
+    BpFast k;
+    float2 *out;
+    int64_t *oow;
+    cudaStream_t s;
+};
+
+template <int VX, int MINB, bool PAIR>
+int launch_tile(const TileArgs &a) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpa_tile_kernel<VX, MINB, PAIR>,
+                                                      TL_THREADS, 0);
+        if (per_sm <= 0) per_sm = 1;
+    }
+    // only tiles intersecting [vb, ve) matter; x-slab sharding keeps that a
+    // contiguous run of tile columns
+    const int64_t plane = (int64_t)a.ny * a.nz;
+    const int tx0 = (int)((a.vb / plane) / VX);
+    const int tx1 = (int)(((a.ve - 1) / plane) / VX);
+    const int64_t per_x = (int64_t)((a.ny + TL_TY - 1) / TL_TY) * ((a.nz + TL_TZ - 1) / TL_TZ);
+    const int64_t tiles = (int64_t)(tx1 - tx0 + 1) * per_x;
+    const int split = tile_split(tiles, a.m, per_sm);
+    float2 *part = nullptr;
+    const int64_t nv = a.ve - a.vb;
+    if (split > 1 && cudaMallocAsync(&part, (split - 1) * nv * sizeof(float2), a.s) != cudaSuccess)
+        return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
+    bpa_tile_kernel<VX, MINB, PAIR><<<(unsigned)(tiles * split), TL_THREADS, 0, a.s>>>(
+        a.origin[0], a.origin[1], a.origin[2], a.step[0], a.step[1], a.step[2], a.nx, a.ny, a.nz,
+        a.vb, a.ve, a.el, a.m, a.env, a.k, a.out, a.oow, tx0, (int)tiles, split, part);
+    if (split > 1) {
+        add_parts_kernel<<<4 * sm_count(), 256, 0, a.s>>>(a.out, part, split - 1, nv);
+        cudaFreeAsync(part, a.s);
+    }
+    return check_launch("bpa_tile_kernel");
 }
 
 BpConst make_bp_const(int64_t n_t, double t0, double dt, double k_ref) {
@@ -394,29 +500,26 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
         k.n_t = c.n_t;
         k.cbin = -0.5f - c.x0;
         k.kfrac = MAGIC - c.x0;
-        // only tiles intersecting [vox_begin, vox_end) matter; x-slab sharding
-        // keeps that a contiguous run of tile columns
-        const int64_t plane = (int64_t)ny * nz;
-        const int tx0 = (int)((vox_begin / plane) / TL_VX);
-        const int tx1 = (int)(((vox_end - 1) / plane) / TL_VX);
-        const int64_t per_x = (int64_t)((ny + TL_TY - 1) / TL_TY) * ((nz + TL_TZ - 1) / TL_TZ);
-        const int64_t tiles = (int64_t)(tx1 - tx0 + 1) * per_x;
-        const int split = tile_split(tiles, m);
-        float2 *part = nullptr;
-        const int64_t nv = vox_end - vox_begin;
-        if (split > 1 && cudaMallocAsync(&part, (split - 1) * nv * sizeof(float2), s) != cudaSuccess)
-            return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
-        bpa_tile_kernel<<<(unsigned)(tiles * split), TL_THREADS, 0, s>>>(
-            origin[0], origin[1], origin[2], step[0], step[1], step[2], nx, ny,
-            nz, vox_begin, vox_end, reinterpret_cast<const float4 *>(el_xyz), (int)m,
-            reinterpret_cast<const float2 *>(envelopes), k, reinterpret_cast<float2 *>(out),
-            oow_total, tx0, (int)tiles, split, part);
-        if (split > 1) {
-            add_parts_kernel<<<4 * sm_count(), 256, 0, s>>>(reinterpret_cast<float2 *>(out), part,
-                                                            split - 1, nv);
-            cudaFreeAsync(part, s);
+        k.alpha_d = k_ref * HHSAR_C_LIGHT * dt;
+        k.alpha = (float)k.alpha_d;
+        k.kc_t0 = k_ref * HHSAR_C_LIGHT * t0;
+        static const int variant = [] {
+            const char *v = getenv("HHSAR_BPA_VARIANT");
+            return v ? atoi(v) : 0;
+        }();
+        const TileArgs a{origin, step, nx, ny, nz, vox_begin, vox_end,
+                         reinterpret_cast<const float4 *>(el_xyz), (int)m,
+                         reinterpret_cast<const float2 *>(envelopes), k,
+                         reinterpret_cast<float2 *>(out), oow_total, s};
+        switch (variant) {
+            // A/B variants (HHSAR_BPA_VARIANT): VX voxels/thread, min CTAs/SM,
+            // packed fp32x2 pair path.  Default measured fastest on B200.
+            case 1: return launch_tile<4, 5, false>(a);
+            case 2: return launch_tile<8, 3, false>(a);
+            case 3: return launch_tile<8, 3, true>(a);
+            case 4: return launch_tile<4, 4, true>(a);
+            default: return launch_tile<4, 5, true>(a);
         }
-        return check_launch("bpa_tile_kernel");
     }
     const int64_t tiles = (int64_t)((nx + CART_V - 1) / CART_V) * ((ny + CART_TY - 1) / CART_TY) *
                           ((nz + CART_TZ - 1) / CART_TZ);

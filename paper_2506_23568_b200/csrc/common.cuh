@@ -134,6 +134,49 @@ __device__ __forceinline__ void cfma(float2 &acc, float2 a, float2 b) {
     acc.y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y));
 }
 
+// ---- packed float32x2 (Blackwell FFMA2 / FADD2 / FMUL2) ---------------------
+// Two independent fp32 lanes per instruction: halves the issue slots of the
+// FMA-pipe work; a scalar operand is broadcast by ptxas (.F32 operand form).
+struct f2x {
+    unsigned long long r;
+};
+__device__ __forceinline__ f2x pk2(float lo, float hi) {
+    f2x v;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v.r) : "f"(lo), "f"(hi));
+    return v;
+}
+__device__ __forceinline__ f2x bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ float lo2(f2x v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
+    return a;
+}
+__device__ __forceinline__ float hi2(f2x v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
+    return b;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.r) : "l"(a.r), "l"(b.r), "l"(c.r));
+    return d;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
+__device__ __forceinline__ f2x sub2(f2x a, f2x b) {
+    f2x d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
+
 // Keys cubic convolution weights, a = -1/2 (_kernels.py:192-200).
 __device__ __forceinline__ void keys_weights(float f, float w[4]) {
     w[0] = ((-0.5f * f + 1.0f) * f - 0.5f) * f;
