@@ -268,6 +268,138 @@ def partition_subarrays(aperture, levels: int) -> SubarrayTree:
     return SubarrayTree(aperture=aperture, levels=tuple(tiers))
 
 
+@dataclass(frozen=True)
+class JitterSpec:
+    """Handheld trajectory uncertainty (model.py:73-88)."""
+
+    depth_amplitude: float = 0.0
+    lateral_sigma: float = 0.0
+
+    def __post_init__(self):
+        if self.depth_amplitude < 0 or self.lateral_sigma < 0:
+            raise ConfigError("jitter amplitudes must be non-negative")
+
+
+def generate_handheld_aperture(nx: int, ny: int, extent: float, jitter=None,
+                               seed: int = 0) -> SyntheticAperture:
+    """Jittered raster scan (model.py:256-308), same seeded draws: lateral
+    Gaussian noise, then a box-smoothed random walk in z' scaled to the
+    depth bound."""
+    if nx < 1 or ny < 1:
+        raise ConfigError("aperture lattice shape must be at least 1x1")
+    if not (extent > 0 and np.isfinite(extent)):
+        raise ConfigError("aperture extent must be positive")
+    jitter = jitter or JitterSpec()
+    xs = np.linspace(-extent / 2, extent / 2, nx) if nx > 1 else np.zeros(1)
+    ys = np.linspace(-extent / 2, extent / 2, ny) if ny > 1 else np.zeros(1)
+    gx, gy = np.meshgrid(xs, ys)
+    n = nx * ny
+    el = np.zeros((n, 3))
+    el[:, 0], el[:, 1] = gx.ravel(), gy.ravel()
+    rng = np.random.default_rng(seed)
+    if jitter.lateral_sigma > 0:
+        el[:, :2] += rng.normal(0.0, jitter.lateral_sigma, (n, 2))
+    if jitter.depth_amplitude > 0:
+        walk = np.cumsum(rng.standard_normal(n))
+        w = max(3, nx)
+        walk = np.convolve(np.pad(walk, w, mode="edge"), np.ones(w) / w, "same")[w:-w]
+        walk -= walk.mean()
+        peak = np.abs(walk).max()
+        if peak > 0:
+            el[:, 2] = walk * (jitter.depth_amplitude / peak)
+    return SyntheticAperture(elements=el, nx=nx, ny=ny)
+
+
+@dataclass(frozen=True)
+class Scene:
+    """Point scatterers (model.py:222-245)."""
+
+    positions: np.ndarray
+    reflectivity: np.ndarray
+
+    def __post_init__(self):
+        p = np.atleast_2d(np.asarray(self.positions, dtype=float))
+        if p.size == 0:
+            p = p.reshape(0, 3)
+        r = np.atleast_1d(np.asarray(self.reflectivity, dtype=complex))
+        if p.ndim != 2 or p.shape[1] != 3:
+            raise ConfigError("scene positions must have shape (n, 3)")
+        if r.shape != (p.shape[0],):
+            raise ConfigError("one reflectivity per scatterer required")
+        if p.size and not np.all(np.isfinite(p)):
+            raise ConfigError("scatterer positions must be finite")
+        object.__setattr__(self, "positions", _frozen(p))
+        object.__setattr__(self, "reflectivity", _frozen(r))
+
+    @property
+    def n_scatterers(self) -> int:
+        return self.positions.shape[0]
+
+
+def scene_grid(shape, spacing: float, center, reflectivity: complex = 1.0) -> Scene:
+    """Regular scatterer lattice (simulator.py:72-94)."""
+    shape = tuple(int(s) for s in shape)
+    if any(s < 1 for s in shape):
+        raise ConfigError("grid shape entries must be at least 1")
+    if spacing < 0:
+        raise ConfigError("grid spacing must be non-negative")
+    axes = [(np.arange(s) - (s - 1) / 2) * spacing + c for s, c in zip(shape, center)]
+    g = np.meshgrid(*axes, indexing="ij")
+    pos = np.stack([a.ravel() for a in g], axis=-1)
+    return Scene(pos, np.full(pos.shape[0], reflectivity, dtype=complex))
+
+
+def scene_star(diameter: float, spokes: int, points_per_spoke: int, center,
+               reflectivity: complex = 1.0) -> Scene:
+    """Radial-spoke target (simulator.py:97-113)."""
+    if diameter <= 0 or spokes < 1 or points_per_spoke < 1:
+        raise ConfigError("star needs positive diameter, spokes, and density")
+    radii = np.linspace(diameter / (2 * (points_per_spoke + 1)), diameter / 2,
+                        points_per_spoke)
+    ang = np.arange(spokes) * (2 * np.pi / spokes)
+    cx, cy, cz = center
+    pos = np.array([(cx + r * np.cos(a), cy + r * np.sin(a), cz) for a in ang for r in radii])
+    return Scene(pos, np.full(pos.shape[0], reflectivity, dtype=complex))
+
+
+def scene_from_spec(spec: dict, region=None) -> Scene:
+    """Scene from a config mapping (simulator.py:116-161): kinds grid, star,
+    points; every scatterer must lie inside ``region`` when given."""
+    if not isinstance(spec, dict) or "kind" not in spec:
+        raise ConfigError("scene spec must be a mapping with a 'kind' entry")
+    kind = spec["kind"]
+    known = {"grid": {"kind", "shape", "spacing", "center", "reflectivity"},
+             "star": {"kind", "diameter", "spokes", "points_per_spoke", "center",
+                      "reflectivity"},
+             "points": {"kind", "positions", "reflectivity"}}
+    if kind not in known:
+        raise ConfigError(f"unknown scene kind '{kind}'")
+    unknown = set(spec) - known[kind]
+    if unknown:
+        raise ConfigError(f"unknown scene fields: {sorted(unknown)}")
+    try:
+        if kind == "grid":
+            scene = scene_grid(spec["shape"], spec["spacing"], spec["center"],
+                               complex(spec.get("reflectivity", 1.0)))
+        elif kind == "star":
+            scene = scene_star(spec["diameter"], spec["spokes"], spec["points_per_spoke"],
+                               spec["center"], complex(spec.get("reflectivity", 1.0)))
+        else:
+            pos = np.asarray(spec["positions"], dtype=float)
+            refl = spec.get("reflectivity", [1.0] * len(pos))
+            if np.isscalar(refl):
+                refl = [refl] * len(pos)
+            scene = Scene(pos, np.asarray(refl, dtype=complex))
+    except KeyError as exc:
+        raise ConfigError(f"scene spec missing field {exc}") from exc
+    if region is not None and scene.n_scatterers:
+        inside = region.contains(scene.positions)
+        if not np.all(inside):
+            bad = scene.positions[~inside][0]
+            raise ConfigError(f"scatterer at {tuple(bad)} lies outside the imaging region")
+    return scene
+
+
 def validate_geometry(aperture, region) -> None:
     """Region must sit strictly in front of every element (model.py:248-253)."""
     z_max = float(np.asarray(aperture.elements)[:, 2].max())

@@ -244,7 +244,41 @@ def case_config0(out):
     _grid_meta("grid", grids, out)
 
 
+RUN_CONFIG = {  # a small desk-like run config in the reference's schema (cli.py:167-190)
+    "aperture": {"nx": 9, "ny": 9, "extent": 0.0375,
+                 "jitter": {"depth_amplitude": 0.0066, "lateral_sigma": 0.000125}},
+    "frequencies": {"start_hz": 12.0e9, "stop_hz": 15.0e9, "count": 16},
+    "region": {"center": [0.0, 0.0, 0.0333], "extents": [0.0417, 0.0417, 0.0417]},
+    "scene": {"kind": "grid", "shape": [3, 3, 3], "spacing": 0.0146,
+              "center": [0.0, 0.0, 0.0333]},
+    "seed": 7,
+    "algorithm": {"name": "hhffbpa", "levels": 3, "oversample": 1.4, "kernel": "linear"},
+    "dims": [17, 17, 9],
+}
+
+
+def case_io():
+    """Files written by the reference's own io.py and CLI: the byte formats
+    and the config schema the drop-in must read and write identically."""
+    import json
+    from hhsar.cli import load_run_config, main as ref_main
+    from hhsar.io import read_volume
+    cfg_path = HERE / "run_config.json"
+    cfg_path.write_text(json.dumps(RUN_CONFIG, indent=1))
+    cube_path = HERE / "io_cube.bin"
+    vol_path = HERE / "io_vol.bin"
+    assert ref_main(["simulate", "--config", str(cfg_path), "--out", str(cube_path)]) == 0
+    assert ref_main(["reconstruct", "--algo", "hhffbpa", "--levels", "3", "--in",
+                     str(cube_path), "--out", str(vol_path), "--dims", "17,17,9"]) == 0
+    cfg = load_run_config(cfg_path)
+    out = {"elements": cfg.build_aperture().elements,
+           "scene_positions": cfg.scene.positions,
+           "volume": read_volume(vol_path).values}
+    np.savez_compressed(HERE / "io_reference.npz", **out)
+
+
 def main():
+    case_io()
     for name, fn in (("small", case_small), ("medium", case_medium), ("config0", case_config0)):
         out = {}
         fn(out)
