@@ -271,10 +271,77 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"], result["parity"] = cpu_baseline_leg(w, out[:ve - vb], dt, k_ref)
+        if world == 1 and not args.no_hhffbpa:
+            result["hhffbpa"] = {f"config{c}": hhffbpa_leg(c, dev, args.steps, check=(c == 2))
+                                 for c in (2, 3)}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def hhffbpa_leg(index, dev, steps, check=False):
+    """HHFFBPA on BASELINE config `index` (binary schedule, the reference's
+    own): device-resident cube, one step = range compression + grids +
+    leaf BPA + merges + Cartesian landing.  BPA-equivalent rate =
+    N_vox * N_el / t (the unit the paper's speed-up is quoted in)."""
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, ffbp, rangecomp, workloads
+    w = workloads.config(index)
+    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                            w.freqs.k_samples, device=dev)
+    el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+    el4 = bpa.el_f32x4(el)
+    params = ffbp.FfbpParams(levels=w.levels)
+
+    def step():
+        env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
+        return ffbp.hhffbpa_device(env, el, el4, 0.0, dt, k_ref, w.freqs, w.region, w.dims,
+                                   params, w.levels, 2)
+
+    for _ in range(3):
+        run = step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        run = step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    stats = run.lattices.stats.cpu().numpy()
+    sched, d = run.sched, run.lattices.descs
+    g0, g1 = sched.level_slices[0]
+    leaf_units = int(sum(int(stats[g, 2]) * int(d["stop"][g] - d["start"][g])
+                         for g in range(g0, g1)))
+    merge_units = sum(int(stats[a:b, 0].sum()) * f
+                      for (a, b), f in zip(sched.level_slices[1:], sched.fanouts))
+    merge_units += w.n_voxels * sched.final_children
+    out = {"workload": f"BASELINE config {index}: {w.n_elements} elements, {w.freqs.count} "
+                       f"freqs, {list(w.dims)} voxels, binary M={w.levels}",
+           "ms_per_step": round(ms, 3), "volumes_per_s": round(1e3 / ms, 2),
+           "bpa_equivalent_gunits_per_s": round(w.bpa_units / (ms / 1e3) / 1e9, 1),
+           "grids": int(sched.n_grids), "leaf_units": leaf_units, "merge_units": merge_units,
+           "newton_iterations": int(stats[:, 4].sum()),
+           "step": "range compression + grid plan/Newton + leaf BPA + merges + landing"}
+    if check:
+        import oracle
+        from paper_2506_23568_b200.model import DataCube
+        host = DataCube(values=cube.cpu().numpy(), aperture=w.aperture, freqs=w.freqs)
+        t = time.perf_counter()
+        want, _, _, prov = oracle.hhffbpa_reconstruct(host, w.region, w.dims, levels=w.levels,
+                                                      upsample=w.upsample)
+        t = time.perf_counter() - t
+        got = run.volume.cpu().numpy().reshape(w.dims)
+        lp = [[int(v) for v in stats[a:b, 2 if k == 0 else 0]]
+              for k, (a, b) in enumerate(sched.level_slices)]
+        out["parity_vs_oracle"] = {
+            "rel_l2": float(np.linalg.norm(got - want) / np.linalg.norm(want)),
+            "peak_index_equal": bool(np.argmax(np.abs(got)) == np.argmax(np.abs(want))),
+            "level_points_equal": lp == prov["level_points"][:-1]}
+        out["cpu_oracle_s"] = round(t, 2)
+        out["cpu_oracle_cores"] = oracle.threads()
+    return out
 
 
 def cpu_baseline_leg(w, gpu_flat, dt, k_ref, planes=(60, 140)):
@@ -393,6 +460,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hhffbpa", action="store_true",
+                    help="skip the HHFFBPA (configs 2 and 3) extra object")
     ap.add_argument("--ref-rows", type=int, default=64,
                     help="reference arm: y-rows (x 64 z-voxels) of one x-plane per step")
     args = ap.parse_args()
