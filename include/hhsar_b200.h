@@ -150,6 +150,12 @@ int hhsar_range_pad(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
  * unnormalised IDFT into demodulated envelopes. */
 int hhsar_range_demod(void *prof, int64_t n_el, int64_t n_t, double a, double dt,
                       float scale, void *stream);
+/* Fused range compression (rangecomp.py:61-101 in one HBM pass): per element
+ * row, zero-pad cube[e][0..n_f) to n_t bins, unnormalised inverse DFT,
+ * multiply by exp(j a (dt i)); out[n_el][n_t] complex64.  n_t must be a
+ * power of two in [16, 8192] (other sizes: cuFFT + hhsar_range_demod). */
+int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t, double a,
+                         double dt, void *out, void *stream);
 
 /* ---- HHFFBPA: grids ------------------------------------------------------ */
 

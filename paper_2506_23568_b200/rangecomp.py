@@ -12,6 +12,7 @@ backprojection kernel reads.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -48,6 +49,13 @@ class RangeProfileSet:
         return (self.t0, self.t0 + (self.n_samples - 1) * self.dt)
 
 
+# The fused single-pass kernel (hhsar_range_compress) is exact to 2e-7 vs the
+# cuFFT path but its radix-4 shared-memory passes are still slower than cuFFT
+# + the demodulation kernel on B200 (config 3: 3.0 vs 2.3 ms), so cuFFT is the
+# default until the register-resident radix-16 version lands.
+_FORCE_CUFFT = os.environ.get("HHSAR_RANGE_FFT", "cufft") != "fused"
+
+
 def profile_axis(freqs, upsample: int):
     """(n_t, dt, k_ref, a) exactly as rangecomp.py:84-96 computes them;
     a = (k_min - k_ref) * c is the demodulation rate per second of delay."""
@@ -81,6 +89,16 @@ def range_compress_device(cube_dev, freqs, upsample: int = 8):
     """Device cube [N_el, n_f] complex64 -> envelopes [N_el, n_t] complex64."""
     import torch
     n_t, dt, k_ref, a = profile_axis(freqs, upsample)
+    if cube_dev.dtype != torch.complex64:
+        cube_dev = cube_dev.to(torch.complex64)
+    if 16 <= n_t <= 8192 and n_t & (n_t - 1) == 0 and not _FORCE_CUFFT:
+        # one fused pass: pad + IDFT + demodulation (hhsar_range_compress)
+        cube_dev = cube_dev.contiguous()
+        prof = torch.empty((cube_dev.shape[0], n_t), dtype=torch.complex64,
+                           device=cube_dev.device)
+        _native.call("hhsar_range_compress", _native.ptr(cube_dev), cube_dev.shape[0],
+                     cube_dev.shape[1], n_t, a, dt, _native.ptr(prof), _native.stream_handle())
+        return prof, dt, k_ref
     prof = torch.fft.ifft(cube_dev, n=n_t, dim=1, norm="forward")
     if prof.dtype != torch.complex64:
         prof = prof.to(torch.complex64)
