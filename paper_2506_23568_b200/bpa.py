@@ -232,8 +232,16 @@ def _finish(vol, oow, dims, origin, step, provenance, extra_flags=None):
     finite = torch.isfinite(torch.view_as_real(vol)).all().reshape(1).to(torch.int64)
     scalars = torch.cat([oow.reshape(-1)[:1], finite] +
                         ([extra_flags.reshape(-1)] if extra_flags is not None else []))
-    host = vol.cpu().numpy().reshape(dims)
-    sc = scalars.cpu().numpy()
+    # pinned destinations (the caching host allocator reuses them across
+    # calls) so both copies are DMA transfers queued behind the kernels; one
+    # stream synchronisation for everything
+    host_t = torch.empty(vol.shape, dtype=vol.dtype, pin_memory=True)
+    sc_t = torch.empty(scalars.shape, dtype=scalars.dtype, pin_memory=True)
+    host_t.copy_(vol, non_blocking=True)
+    sc_t.copy_(scalars, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    host = host_t.numpy().reshape(dims)
+    sc = sc_t.numpy()
     if int(sc[0]):
         raise NumericDomainError(
             f"{int(sc[0])} point-element delays fell outside the profile window; "

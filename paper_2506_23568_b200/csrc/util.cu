@@ -29,6 +29,15 @@ int sm_count() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
         if (cached <= 0) cached = 148;
+        // Scratch buffers come from the stream-ordered pool (cudaMallocAsync);
+        // keep freed blocks cached instead of returning them to the driver at
+        // every synchronisation (threshold 0 by default), so repeated
+        // reconstructions do not pay a cudaMalloc per call.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     return cached;
 }
