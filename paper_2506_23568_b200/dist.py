@@ -14,8 +14,11 @@ sharding and reassembly logic is tested with gloo on CPU
 
 from __future__ import annotations
 
+from types import SimpleNamespace
+
 import numpy as np
 
+from .errors import ConfigError
 from .bpa import (_finish, bpa_volume_device, check_delay_window, default_grid_dims,
                   el_f32x4, region_grid)
 from .model import validate_geometry
@@ -82,6 +85,236 @@ def bpa_reconstruct_sharded(cube, region, dims=None, upsample: int = 8, group=No
     oow = _allreduce_sum(oows[0], group)
     return _finish(flat, oow, dims, origin, step,
                    {"algorithm": "bpa", "upsample": upsample, "dims": list(dims)})[0]
+
+
+# ---------------------------------------------------------------------------
+# HHFFBPA across GPUs
+# ---------------------------------------------------------------------------
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def _raw(self, t):
+        import torch
+        return torch.view_as_real(t) if t.is_complex() else t
+
+    def allreduce_sum(self, t) -> None:
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+
+    def allgather_segments(self, buf, segments) -> None:
+        """buf[a_r:b_r] holds rank r's data on rank r; afterwards every rank
+        holds every segment (one all_gather of equal padded chunks)."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        longest = max(b - a for a, b in segments)
+        a, b = segments[self.rank]
+        send = torch.zeros(longest, dtype=buf.dtype, device=buf.device)
+        send[:b - a] = buf[a:b]
+        recv = torch.empty(longest * self.world, dtype=buf.dtype, device=buf.device)
+        dist.all_gather_into_tensor(self._raw(recv), self._raw(send), group=self.group)
+        for r, (a, b) in enumerate(segments):
+            if r != self.rank:
+                buf[a:b] = recv[r * longest: r * longest + (b - a)]
+
+
+class EmulatedComm:
+    """World of `world` ranks emulated by host threads in one process on one
+    GPU (for tests): each rank runs its own pipeline; collectives exchange
+    tensors through host-side barriers -- no kernel ever waits on another."""
+
+    def __init__(self, rank: int, world: int, shared: dict):
+        import threading
+        self.rank, self.world = rank, world
+        self.shared = shared
+        shared.setdefault("barrier", threading.Barrier(world))
+        shared.setdefault("slots", [None] * world)
+
+    def _exchange(self, t):
+        import torch
+        torch.cuda.synchronize()
+        self.shared["slots"][self.rank] = t
+        self.shared["barrier"].wait()
+        out = list(self.shared["slots"])
+        self.shared["barrier"].wait()
+        return out
+
+    def allreduce_sum(self, t) -> None:
+        parts = self._exchange(t.clone())
+        total = parts[0].clone()
+        for p in parts[1:]:
+            total += p
+        t.copy_(total)
+
+    def allgather_segments(self, buf, segments) -> None:
+        a, b = segments[self.rank]
+        parts = self._exchange(buf[a:b].clone())
+        for r, (a, b) in enumerate(segments):
+            if r != self.rank:
+                buf[a:b] = parts[r]
+
+
+def exchange_level(sched, world: int):
+    """Highest grid level (index into sched.level_slices) whose subimage
+    count is a multiple of `world`: each rank owns count/world consecutive
+    subtrees below it.  None when no level splits evenly."""
+    best = None
+    for k, (a, b) in enumerate(sched.level_slices):
+        if (b - a) % world == 0 and b - a >= world:
+            best = k
+    return best
+
+
+def plan_shard(n_elements: int, levels: int, merge_factor: int, world: int, rank: int):
+    """(schedule, exchange level kx, owned grid slices per level <= kx,
+    owned element rows [e0, e1)).  kx = -1 when no level splits evenly (then
+    every rank builds every subtree and only the landing is sharded)."""
+    from .ffbp import Schedule
+    sched = Schedule(n_elements, levels, merge_factor)
+    n_lv = len(sched.level_slices)
+    kx = exchange_level(sched, world) if world > 1 else n_lv - 1
+    if kx is None:
+        return sched, -1, list(sched.level_slices), (0, n_elements)
+    owned = []
+    for k in range(kx + 1):
+        a, b = sched.level_slices[k]
+        per = (b - a) // world
+        owned.append((a + rank * per, a + (rank + 1) * per))
+    g0, g1 = owned[0]
+    e0 = int(sched.grids["start"][g0])
+    e1 = int(sched.grids["stop"][g1 - 1])
+    return sched, kx, owned, (e0, e1)
+
+
+def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsample: int = 8,
+                                merge_factor: int = 2, comm=None):
+    """hhffbpa_reconstruct (ffbp.py:415-513) over all ranks of `comm`
+    (default: torch.distributed's world).  Every rank returns the same
+    ImageVolume and provenance; each rank transfers and range-compresses only
+    its own subaperture group's echoes."""
+    import torch
+    from .bpa import _finish, check_delay_window, default_grid_dims, region_grid
+    from .ffbp import FfbpParams, check_grids, default_levels, provenance_of
+    from .model import partition_subarrays, validate_geometry
+    from .rangecomp import RangeProfileSet, profile_axis, to_device_cube
+    comm = comm or TorchComm()
+    params = params or FfbpParams()
+    validate_geometry(cube.aperture, region)
+    kgrid = cube.freqs
+    dims = tuple(int(d) for d in (final_dims or default_grid_dims(region, kgrid)))
+    levels = params.levels if params.levels is not None else default_levels(cube.aperture)
+    if levels < 2:
+        raise ConfigError("the sharded HHFFBPA needs levels >= 2 (levels=1 is the BPA: "
+                          "use bpa_reconstruct_sharded)")
+    if region.z_min <= 0.0:
+        raise ConfigError("region must sit strictly in front of the array")
+    partition_subarrays(cube.aperture, levels)
+    n_el = cube.aperture.n_elements
+    _, _, _, (e0, e1) = plan_shard(n_el, levels, merge_factor, comm.world, comm.rank)
+    el_dev = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
+                          device="cuda")
+    n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
+    window = RangeProfileSet(envelopes=torch.empty((0, n_t)), t0=0.0, dt=dt,
+                             upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
+                             freqs=kgrid, elements_dev=el_dev)
+    check_delay_window(window, region)
+    rows = to_device_cube(np.asarray(cube.values)[e0:e1])
+    vol, stats, flags, oow, sched, descs = hhffbpa_sharded_device(
+        comm, rows, e0, el_dev, kgrid, region, dims, params, levels, merge_factor, upsample)
+    origin, step = region_grid(region, dims)
+    extra = torch.cat([flags, stats.reshape(-1)])
+    volume, tail = _finish(vol, oow, dims, origin, step, {}, extra)
+    fl = tail[:flags.numel()]
+    st = tail[flags.numel():].reshape(-1, stats.shape[1])
+    run = SimpleNamespace(sched=sched, lattices=SimpleNamespace(descs=descs))
+    check_grids(run, st)
+    prov = provenance_of(run, st, fl, dims, params, levels, upsample, merge_factor)
+    object.__setattr__(volume, "provenance", prov)
+    return volume
+
+
+def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, region, final_dims,
+                           params, levels: int, merge_factor: int, upsample: int):
+    """One rank's share of HHFFBPA:
+
+    1. subaperture-group partition: the rank owns a contiguous run of
+       subtrees up to the exchange level and range-compresses only those
+       elements (``cube_dev_rows`` = its rows, starting at ``e_row0``);
+       every grid is PLANNED for the whole region on every rank (so lattices
+       are identical to the 1-GPU ones), Newton runs only where this rank
+       evaluates points;
+    2. all-gather of the exchange level's downconverted lattices (NCCL);
+    3. the few top merge levels redundantly on every rank;
+    4. the Cartesian landing voxel-sharded, then an all-gather of the slabs.
+
+    Returns (flat complex64 volume, stats[G,6], flags, oow) identical on all
+    ranks.
+    """
+    import torch
+    from .bpa import el_f32x4
+    from .ffbp import Pipeline
+    from .rangecomp import range_compress_device
+    env, dt, k_ref = range_compress_device(cube_dev_rows, kgrid, upsample)
+    world, rank = comm.world, comm.rank
+    sched, kx, owned, _ = plan_shard(el_dev.shape[0], levels, merge_factor, world, rank)
+    n_lv = len(sched.level_slices)
+    mask = np.zeros(sched.n_grids, dtype=bool)
+    for k in range(n_lv):
+        a, b = owned[k] if k <= kx else sched.level_slices[k]
+        mask[a:b] = True
+    pipe = Pipeline(env, el_dev, el_f32x4(el_dev), 0.0, dt, k_ref, kgrid, region, final_dims,
+                    params, levels, merge_factor, newton_grids=mask, env_row0=e_row0,
+                    sched=sched)
+    pipe.leaves(*owned[0])
+    for k in range(max(kx, 0)):
+        pipe.merge(k, *owned[k + 1])
+    if kx >= 0 and world > 1:
+        a, b = sched.level_slices[kx]
+        per = (b - a) // world
+        off = pipe.lat.descs["offset"].astype(np.int64)
+        npts = pipe.lat.npts
+        segs = [(int(off[a + r * per]), int(off[a + (r + 1) * per - 1] + npts[a + (r + 1) * per - 1]))
+                for r in range(world)]
+        comm.allgather_segments(pipe.values, segs)
+    for k in range(max(kx, 0), pipe.n_stages):
+        pipe.merge(k)
+    n_vox = int(np.prod(final_dims))
+    vb, ve = shard_range(n_vox, rank, world)
+    part = pipe.land((vb, ve))
+    # volume slabs
+    vol = torch.zeros(n_vox, dtype=torch.complex64, device=part.device)
+    vol[vb:ve] = part
+    comm.allgather_segments(vol, [shard_range(n_vox, r, world) for r in range(world)])
+    # counters: rows / stages computed by owners are summed, redundant ones kept
+    stats = pipe.lat.stats
+    if world > 1 and kx >= 0:
+        low = stats.clone()
+        g_hi = sched.level_slices[kx][1]
+        low[g_hi:] = 0
+        comm.allreduce_sum(low)
+        stats = torch.cat([low[:g_hi], stats[g_hi:]])
+        fl = pipe.flags.clone()
+        fl[kx:pipe.n_stages] = 0
+        comm.allreduce_sum(fl)
+        flags = torch.cat([fl[:kx], pipe.flags[kx:pipe.n_stages], fl[pipe.n_stages:]])
+        oow = pipe.oow.clone()
+        comm.allreduce_sum(oow)
+    else:
+        flags = pipe.flags.clone()
+        fl = flags[pipe.n_stages:].clone()
+        comm.allreduce_sum(fl)
+        flags[pipe.n_stages:] = fl
+        oow = pipe.oow
+    return vol, stats, flags, oow, sched, pipe.lat.descs
 
 
 def _allreduce_sum(t, group=None):

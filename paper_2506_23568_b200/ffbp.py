@@ -174,8 +174,16 @@ class Lattices:
 
 
 def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float,
-                   pad: int, window_hi: float, tol: float = 1e-9, max_iter: int = 50) -> Lattices:
-    """Plan + Newton for every grid of the schedule (ffbp.py:179-307)."""
+                   pad: int, window_hi: float, tol: float = 1e-9, max_iter: int = 50,
+                   newton_grids=None) -> Lattices:
+    """Plan + Newton for every grid of the schedule (ffbp.py:179-307).
+
+    Every grid is planned (metadata is cheap and needed by any rank that
+    merges it); ``newton_grids`` (bool per grid) restricts the Newton
+    inversion to the grids this process will actually evaluate points of
+    (multi-GPU subtree ownership).  Unselected grids keep valid = 0 and zero
+    counters.
+    """
     import torch
     dev = el_dev.device
     stream = _native.stream_handle()
@@ -200,6 +208,8 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     # Newton work list: the active (u, v) rectangle of every grid
     span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
     cols = span[:, 0] * span[:, 1]
+    if newton_grids is not None:
+        cols = np.where(np.asarray(newton_grids, dtype=bool), cols, 0)
     starts = np.concatenate([[0], np.cumsum(cols)[:-1]])
     host["col_offset"] = starts
     n_cols = int(cols.sum())
@@ -226,49 +236,102 @@ class DeviceRun:
     oow: object               # int64 [1]
 
 
+class Pipeline:
+    """The fused HHFFBPA stages on device-resident envelopes, callable on
+    grid subsets (the multi-GPU driver in dist.py runs each rank's subtrees).
+
+    ``env`` holds envelope rows [env_row0, env_row0 + env.shape[0]) of the
+    aperture; kernels index rows by global element number, so the pointer
+    handed to them is shifted back by env_row0 rows (only owned rows are
+    ever dereferenced).
+    """
+
+    def __init__(self, env, el_dev, el4, t0: float, dt: float, k_ref: float, kgrid, region,
+                 final_dims, params: FfbpParams, levels: int, merge_factor: int = 2,
+                 window_hi=None, newton_grids=None, env_row0: int = 0, sched=None):
+        import ctypes
+        import torch
+        self.dev = env.device
+        self.env, self.el4 = env, el4
+        self.t0, self.dt, self.k_ref = float(t0), float(dt), float(k_ref)
+        self.region, self.final_dims, self.params = region, tuple(final_dims), params
+        self.kid = _kernel_id(params.kernel)
+        src_pad = GRID_PAD + (3 if params.kernel == "cubic" else 2)  # ffbp.py:468
+        if window_hi is None:
+            window_hi = t0 + (env.shape[1] - 1) * dt
+        self.sched = sched or Schedule(el_dev.shape[0], levels, merge_factor)
+        self.lat = build_lattices(el_dev, self.sched, region, kgrid, params.gamma, params.margin,
+                                  src_pad, window_hi, newton_grids=newton_grids)
+        self.values = torch.empty(int(self.lat.npts.sum()), dtype=torch.complex64,
+                                  device=self.dev)
+        self.lat.values = self.values
+        self.n_stages = len(self.sched.fanouts)
+        self.flags = torch.zeros(self.n_stages + 1, dtype=torch.int64, device=self.dev)
+        self.oow = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.env_ptr = ctypes.c_void_p(env.data_ptr() - int(env_row0) * env.shape[1] * 8)
+
+    def leaves(self, g0=None, g1=None):
+        """Level-1 subimages of leaf grids [g0, g1) (default: all)."""
+        a, b = self.sched.level_slices[0]
+        g0 = a if g0 is None else g0
+        g1 = b if g1 is None else g1
+        if g1 <= g0:
+            return
+        lat = self.lat
+        _native.call("hhsar_leaf_bp", lat.desc_ptr(g0), g1 - g0, _native.ptr(lat.positions),
+                     _native.ptr(lat.valid), _native.ptr(self.el4), self.env_ptr,
+                     self.env.shape[1], self.t0, self.dt, self.k_ref, _native.ptr(lat.geom), 1,
+                     _native.ptr(self.values), _native.ptr(self.oow), _native.stream_handle())
+
+    def merge(self, k: int, p0=None, p1=None):
+        """Merge stage k: parents [p0, p1) of grid level k+1 (default: all)
+        from their children at grid level k."""
+        fan = self.sched.fanouts[k]
+        c0, _ = self.sched.level_slices[k]
+        a, b = self.sched.level_slices[k + 1]
+        p0 = a if p0 is None else p0
+        p1 = b if p1 is None else p1
+        if p1 <= p0:
+            return
+        lat = self.lat
+        ch0 = c0 + (p0 - a) * fan
+        _native.call("hhsar_merge_level", lat.desc_ptr(p0), p1 - p0, lat.points_in(p0, p1),
+                     _native.ptr(lat.positions), _native.ptr(lat.valid), lat.desc_ptr(ch0),
+                     (p1 - p0) * fan, fan, _native.ptr(self.values), _native.ptr(lat.geom),
+                     self.kid, 1, _native.ptr(self.values),
+                     _native.c_void_p_offset(self.flags, k), _native.stream_handle())
+
+    def land(self, vox_range=None):
+        """Final Cartesian landing of voxels [vb, ve) (default: all)."""
+        import torch
+        origin, step = region_grid(self.region, self.final_dims)
+        n_vox = int(np.prod(self.final_dims))
+        vb, ve = vox_range if vox_range is not None else (0, n_vox)
+        vol = torch.empty(ve - vb, dtype=torch.complex64, device=self.dev)
+        c0, c1 = self.sched.level_slices[-1]
+        d = np.asarray(self.final_dims, dtype=np.int64)
+        _native.call("hhsar_merge_cartesian", _native.ptr(np.ascontiguousarray(origin)),
+                     _native.ptr(np.ascontiguousarray(step)), _native.ptr(d), vb, ve,
+                     self.lat.desc_ptr(c0), c1 - c0, _native.ptr(self.values),
+                     _native.ptr(self.lat.geom), self.kid, _native.ptr(vol),
+                     _native.c_void_p_offset(self.flags, self.n_stages), _native.stream_handle())
+        return vol
+
+    def run(self, vox_range=None) -> DeviceRun:
+        self.leaves()
+        for k in range(self.n_stages):
+            self.merge(k)
+        vol = self.land(vox_range)
+        return DeviceRun(volume=vol, lattices=self.lat, sched=self.sched, flags=self.flags,
+                         oow=self.oow)
+
+
 def hhffbpa_device(env, el_dev, el4, t0: float, dt: float, k_ref: float, kgrid, region,
                    final_dims, params: FfbpParams, levels: int, merge_factor: int = 2,
                    vox_range=None, window_hi=None) -> DeviceRun:
     """The fused HHFFBPA pipeline on device-resident envelopes (levels >= 2)."""
-    import torch
-    dev = env.device
-    stream = _native.stream_handle()
-    kid = _kernel_id(params.kernel)
-    src_pad = GRID_PAD + (3 if params.kernel == "cubic" else 2)  # ffbp.py:468
-    if window_hi is None:
-        window_hi = t0 + (env.shape[1] - 1) * dt
-    sched = Schedule(el_dev.shape[0], levels, merge_factor)
-    lat = build_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin, src_pad,
-                         window_hi)
-    total = int(lat.npts.sum())
-    values = torch.empty(total, dtype=torch.complex64, device=dev)
-    lat.values = values
-    n_stages = len(sched.fanouts)
-    flags = torch.zeros(n_stages + 1, dtype=torch.int64, device=dev)
-    oow = torch.zeros(1, dtype=torch.int64, device=dev)
-    g0, g1 = sched.level_slices[0]
-    _native.call("hhsar_leaf_bp", lat.desc_ptr(g0), g1 - g0, _native.ptr(lat.positions),
-                 _native.ptr(lat.valid), _native.ptr(el4), _native.ptr(env), env.shape[1],
-                 float(t0), float(dt), float(k_ref), _native.ptr(lat.geom), 1,
-                 _native.ptr(values), _native.ptr(oow), stream)
-    for k, fan in enumerate(sched.fanouts):
-        c0, c1 = sched.level_slices[k]
-        p0, p1 = sched.level_slices[k + 1]
-        _native.call("hhsar_merge_level", lat.desc_ptr(p0), p1 - p0, lat.points_in(p0, p1),
-                     _native.ptr(lat.positions), _native.ptr(lat.valid), lat.desc_ptr(c0),
-                     c1 - c0, fan, _native.ptr(values), _native.ptr(lat.geom), kid, 1,
-                     _native.ptr(values), _native.c_void_p_offset(flags, k), stream)
-    origin, step = region_grid(region, final_dims)
-    n_vox = int(np.prod(final_dims))
-    vb, ve = vox_range if vox_range is not None else (0, n_vox)
-    vol = torch.empty(ve - vb, dtype=torch.complex64, device=dev)
-    c0, c1 = sched.level_slices[-1]
-    d = np.asarray(final_dims, dtype=np.int64)
-    _native.call("hhsar_merge_cartesian", _native.ptr(np.ascontiguousarray(origin)),
-                 _native.ptr(np.ascontiguousarray(step)), _native.ptr(d), vb, ve,
-                 lat.desc_ptr(c0), c1 - c0, _native.ptr(values), _native.ptr(lat.geom), kid,
-                 _native.ptr(vol), _native.c_void_p_offset(flags, n_stages), stream)
-    return DeviceRun(volume=vol, lattices=lat, sched=sched, flags=flags, oow=oow)
+    return Pipeline(env, el_dev, el4, t0, dt, k_ref, kgrid, region, final_dims, params, levels,
+                    merge_factor, window_hi).run(vox_range)
 
 
 def _core_masked(desc, n_valid_core) -> float:

@@ -54,6 +54,45 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
+def _comm_worker(rank, world, port, out_path):
+    sys.path.insert(0, str(REPO))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_23568_b200.dist import TorchComm, plan_shard
+    comm = TorchComm()
+    # uneven complex segments: rank r owns [starts[r], starts[r+1])
+    starts = [0, 5, 17, 18, 30][:world + 1]
+    buf = torch.zeros(starts[-1], dtype=torch.complex64)
+    a, b = starts[rank], starts[rank + 1]
+    buf[a:b] = torch.arange(a, b, dtype=torch.float32) * (1 + 1j)
+    comm.allgather_segments(buf, list(zip(starts[:-1], starts[1:])))
+    cnt = torch.tensor([rank + 1, 10 * rank], dtype=torch.int64)
+    comm.allreduce_sum(cnt)
+    # the subtree plan every rank derives must tile the leaves / elements
+    plans = [plan_shard(1000, 8, 2, world, r) for r in range(world)]
+    if rank == 0:
+        np.save(out_path, {"buf": buf.numpy(), "cnt": cnt.numpy(),
+                           "rows": [p[3] for p in plans], "kx": [p[1] for p in plans]},
+                allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_comm_segments_allreduce_and_plan(tmp_path, world):
+    out = tmp_path / "r.npy"
+    mp.start_processes(_comm_worker, args=(world, _free_port(), str(out)), nprocs=world,
+                       start_method="spawn", join=True)
+    res = np.load(out, allow_pickle=True).item()
+    n = [0, 5, 17, 18, 30][world]
+    assert np.array_equal(res["buf"], np.arange(n) * (1 + 1j))
+    assert list(res["cnt"]) == [sum(range(1, world + 1)), 10 * sum(range(world))]
+    rows = res["rows"]
+    assert rows[0][0] == 0 and rows[-1][1] == 1000
+    assert all(rows[r][1] == rows[r + 1][0] for r in range(world - 1))
+    assert len(set(res["kx"])) == 1 and res["kx"][0] >= 0
+
+
 @pytest.mark.parametrize("world", [2])
 def test_voxel_sharded_gather_reassembles_volume(tmp_path, world):
     out = tmp_path / "vol.npy"
