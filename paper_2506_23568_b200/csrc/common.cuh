@@ -77,6 +77,25 @@ __device__ __forceinline__ bool llt_exact(const double *ext, const hhsar_geom &g
     return !(rad <= xmul(gap, 1e-12));
 }
 
+// ---- SFU-seeded float64 rsqrt / reciprocal --------------------------------------
+// fp32 MUFU seed (relative error < 2^-22) refined by ONE float64 Newton step:
+// relative error ~1.5 e0^2 < 1e-13.  Used where a float64 result feeds a
+// tolerance far above 1e-13 (Newton residuals, merge coordinates and phases),
+// never on the bit-exact lattice-metadata path.  Inputs must lie in the fp32
+// normal range (squared distances of metres: fine).
+__device__ __forceinline__ double rsqrt_d(double a) {
+    const double y = (double)rsqrtf((float)a);
+    const double e = fma(-(a * y), y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+
+__device__ __forceinline__ double rcp_d(double a) {
+    const double y = (double)__frcp_rn((float)a);
+    return fma(y, fma(-a, y, 1.0), y);
+}
+
+__device__ __forceinline__ double sqrt_d(double a) { return a * rsqrt_d(a); }
+
 // ---- fast float64 geometry for the merge stages ------------------------------
 // Same formulas, FMA allowed (not on a bit-exactness path).
 struct LltPhase {
@@ -94,11 +113,11 @@ __device__ __forceinline__ LltPhase llt_phase(const double *ext, double gap, dou
     const double xa = ax * ax, xb = bx * bx, ya = ay * ay, yb = by * by;
     const double dy0 = (y - y0) * (y - y0), dx0 = (x - x0) * (x - x0);
     LltPhase o;
-    o.u = c_uv * (sqrt(xa + dy0 + z2) - sqrt(xb + dy0 + z2));
-    o.v = c_uv * (sqrt(dx0 + ya + z2) - sqrt(dx0 + yb + z2));
-    const double r = ((sqrt(xa + ya + z2) + sqrt(xa + yb + z2)) + sqrt(xb + ya + z2))
-                     + sqrt(xb + yb + z2);
-    const double sq = sqrt(r * r - gap);
+    o.u = c_uv * (sqrt_d(xa + dy0 + z2) - sqrt_d(xb + dy0 + z2));
+    o.v = c_uv * (sqrt_d(dx0 + ya + z2) - sqrt_d(dx0 + yb + z2));
+    const double r = ((sqrt_d(xa + ya + z2) + sqrt_d(xa + yb + z2)) + sqrt_d(xb + ya + z2))
+                     + sqrt_d(xb + yb + z2);
+    const double sq = sqrt_d(r * r - gap);
     o.n = c_nhi * sq - c_nlo * r;
     o.phi = 0.25 * k_max * sq + 0.25 * k_min * r;
     return o;
@@ -109,9 +128,9 @@ __device__ __forceinline__ double sdc_phase_fast(const double *ext, double gap, 
     const double z2 = z * z;
     const double ax = x - ext[0], bx = x - ext[1], ay = y - ext[2], by = y - ext[3];
     const double xa = ax * ax, xb = bx * bx, ya = ay * ay, yb = by * by;
-    const double r = ((sqrt(xa + ya + z2) + sqrt(xa + yb + z2)) + sqrt(xb + ya + z2))
-                     + sqrt(xb + yb + z2);
-    return 0.25 * k_max * sqrt(r * r - gap) + 0.25 * k_min * r;
+    const double r = ((sqrt_d(xa + ya + z2) + sqrt_d(xa + yb + z2)) + sqrt_d(xb + ya + z2))
+                     + sqrt_d(xb + yb + z2);
+    return 0.25 * k_max * sqrt_d(r * r - gap) + 0.25 * k_min * r;
 }
 
 // exp(j * phi) for a float64 phase of any size: explicit float64 reduction
