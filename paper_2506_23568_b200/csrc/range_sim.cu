@@ -53,70 +53,189 @@ __global__ void rc_tables_kernel(float2 *__restrict__ roots, float2 *__restrict_
     demod[i] = cis_reduced(a * (dt * (double)i));   // rangecomp.py:95-96
 }
 
+// Register-resident inverse DFTs (y_k = sum_n x_n e^{+2 pi i n k / R}), built
+// as radix-2 splits down to the radix-4 butterfly; fully unrolled.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+// e^{+2 pi i q / R} for R in {8, 16}, q < R/2 (literal constants once unrolled)
+template <int R>
+__device__ __forceinline__ float2 root_of_unity(int q) {
+    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508977f;
+    constexpr float r2 = 0.70710678118654752f;
+    if constexpr (R == 8) {
+        switch (q) {
+            case 0: return make_float2(1.f, 0.f);
+            case 1: return make_float2(r2, r2);
+            case 2: return make_float2(0.f, 1.f);
+            default: return make_float2(-r2, r2);
+        }
+    } else {
+        switch (q) {
+            case 0: return make_float2(1.f, 0.f);
+            case 1: return make_float2(c1, s1);
+            case 2: return make_float2(r2, r2);
+            case 3: return make_float2(s1, c1);
+            case 4: return make_float2(0.f, 1.f);
+            case 5: return make_float2(-s1, c1);
+            case 6: return make_float2(-r2, r2);
+            default: return make_float2(-c1, s1);
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void idft(float2 (&v)[R]) {
+    if constexpr (R == 1) {
+        return;
+    } else if constexpr (R == 2) {
+        const float2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+        const float2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
+        v[0] = cadd(s02, s13);
+        v[1] = make_float2(d02.x - d13.y, d02.y + d13.x);  // d02 + i d13
+        v[2] = csub(s02, s13);
+        v[3] = make_float2(d02.x + d13.y, d02.y - d13.x);  // d02 - i d13
+    } else {
+        constexpr int H = R / 2;
+        float2 e[H], o[H];
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            e[q] = v[2 * q];
+            o[q] = v[2 * q + 1];
+        }
+        idft<H>(e);
+        idft<H>(o);
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            const float2 t = cmul(o[q], root_of_unity<R>(q));
+            v[q] = cadd(e[q], t);
+            v[q + H] = csub(e[q], t);
+        }
+    }
+}
+
+__device__ __forceinline__ int rc_pad(int i) { return i + (i >> 4); }  // breaks stride-16 bank conflicts
+
+// One Stockham pass of radix R on the rows held in shared memory (or read
+// from / written to global memory on the first / last pass).
+template <int N, int R, bool FIRST, bool LAST>
+__device__ __forceinline__ void rc_pass(int j, int ns, float2 *buf, const float2 *__restrict__ src,
+                                        int n_f, bool live, const float2 *__restrict__ roots,
+                                        const float2 *__restrict__ demod, float2 *__restrict__ dst) {
+    float2 v[R];
+    const int k = j & (ns - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = j + r * (N / R);
+        if (FIRST)
+            v[r] = (live && i < n_f) ? __ldg(src + i) : make_float2(0.f, 0.f);
+        else
+            v[r] = buf[rc_pad(i)];
+    }
+    if (!FIRST) {
+        const int t = k * (N / (ns * R));  // twiddle exponent step, units of 2 pi / N
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(roots + t * r));
+    }
+    idft<R>(v);
+    if (LAST) {
+        // ns * R == N: j < ns, outputs land at j + r * N / R (coalesced)
+        if (live) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int i = j + r * (N / R);
+                dst[i] = cmul(v[r], __ldg(demod + i));
+            }
+        }
+    } else {
+        __syncthreads();  // every read of this pass precedes any write
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[rc_pad(base + r * ns)] = v[r];
+        __syncthreads();
+    }
+}
+
 template <int LOGN>
-__global__ void __launch_bounds__(RC_THREADS)
-range_compress_kernel(const float2 *__restrict__ cube, int n_f, const float2 *__restrict__ roots,
-                      const float2 *__restrict__ demod, float2 *__restrict__ out) {
-    constexpr int N = 1 << LOGN;
+struct RcShape {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int T = N >= 16 ? N / 16 : 1;       // threads per row
+    static constexpr int ROWS = T >= 256 ? 1 : 256 / T;  // rows per CTA
+    static constexpr int NP = N + N / 16;                // padded row in smem
+    static constexpr int REM = LOGN % 4;                 // radix 2^REM first pass
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(512)
+range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
+                      const float2 *__restrict__ roots, const float2 *__restrict__ demod,
+                      float2 *__restrict__ out) {
+    using S = RcShape<LOGN>;
+    constexpr int N = S::N, T = S::T;
     extern __shared__ float2 rc_smem[];
-    float2 *in = rc_smem, *tmp = rc_smem + N;
-    const int64_t row = blockIdx.x;
-    const float2 *src = cube + row * n_f;
-    for (int i = threadIdx.x; i < N; i += RC_THREADS)
-        in[i] = i < n_f ? src[i] : make_float2(0.f, 0.f);
-    __syncthreads();
-    int ns = 1;
-    if (LOGN & 1) {  // one radix-2 pass first
-        for (int j = threadIdx.x; j < N / 2; j += RC_THREADS) {
-            const float2 v0 = in[j], v1 = in[j + N / 2];
-            tmp[2 * j] = make_float2(v0.x + v1.x, v0.y + v1.y);
-            tmp[2 * j + 1] = make_float2(v0.x - v1.x, v0.y - v1.y);
-        }
-        __syncthreads();
-        float2 *t = in;
-        in = tmp;
-        tmp = t;
-        ns = 2;
-    }
-    for (; ns < N; ns *= 4) {
-        for (int j = threadIdx.x; j < N / 4; j += RC_THREADS) {
-            const int k = j & (ns - 1);              // j % ns
-            const int tw = k * (N / (4 * ns));        // twiddle step in units of 2 pi / N
-            float2 v0 = in[j], v1 = in[j + N / 4], v2 = in[j + N / 2], v3 = in[j + 3 * N / 4];
-            v1 = cmul(v1, roots[tw]);
-            v2 = cmul(v2, roots[2 * tw]);
-            v3 = cmul(v3, roots[3 * tw]);
-            // inverse radix-4 butterfly: y_r = sum_q v_q i^{q r}
-            const float2 s02 = make_float2(v0.x + v2.x, v0.y + v2.y);
-            const float2 d02 = make_float2(v0.x - v2.x, v0.y - v2.y);
-            const float2 s13 = make_float2(v1.x + v3.x, v1.y + v3.y);
-            const float2 d13 = make_float2(v1.x - v3.x, v1.y - v3.y);
-            const int base = (j - k) * 4 + k;         // (j / ns) * ns * 4 + j % ns
-            tmp[base] = make_float2(s02.x + s13.x, s02.y + s13.y);
-            tmp[base + ns] = make_float2(d02.x - d13.y, d02.y + d13.x);      // + i d13
-            tmp[base + 2 * ns] = make_float2(s02.x - s13.x, s02.y - s13.y);
-            tmp[base + 3 * ns] = make_float2(d02.x + d13.y, d02.y - d13.x);  // - i d13
-        }
-        __syncthreads();
-        float2 *t = in;
-        in = tmp;
-        tmp = t;
-    }
+    const int tx = threadIdx.x % T, ty = threadIdx.x / T;
+    const int64_t row = (int64_t)blockIdx.x * S::ROWS + ty;
+    const bool live = row < n_el;
+    float2 *buf = rc_smem + ty * S::NP;
+    const float2 *src = cube + (live ? row : 0) * n_f;
     float2 *dst = out + row * N;
-    for (int i = threadIdx.x; i < N; i += RC_THREADS) dst[i] = cmul(in[i], __ldg(demod + i));
+    constexpr int P16 = LOGN / 4;  // radix-16 passes
+    int ns = 1;
+    if constexpr (S::REM > 0) {
+        constexpr int R0 = 1 << S::REM;
+#pragma unroll
+        for (int m = 0; m < 16 / R0; ++m)  // N/R0 butterflies over T = N/16 threads
+            if constexpr (P16 == 0) {
+                rc_pass<N, R0, true, true>(tx + m * T, 1, buf, src, n_f, live, roots, demod, dst);
+            } else {
+                // first pass: butterflies j, stores without the trailing sync
+                const int j = tx + m * T;
+                float2 v[R0];
+#pragma unroll
+                for (int r = 0; r < R0; ++r) {
+                    const int i = j + r * (N / R0);
+                    v[r] = (live && i < n_f) ? __ldg(src + i) : make_float2(0.f, 0.f);
+                }
+                idft<R0>(v);
+#pragma unroll
+                for (int r = 0; r < R0; ++r) buf[rc_pad(j * R0 + r)] = v[r];
+            }
+        ns = R0;
+        if constexpr (P16 > 0) __syncthreads();
+    }
+#pragma unroll
+    for (int p = 0; p < P16; ++p) {
+        const bool first = S::REM == 0 && p == 0, last = p == P16 - 1;
+        if (first && last)
+            rc_pass<N, 16, true, true>(tx, ns, buf, src, n_f, live, roots, demod, dst);
+        else if (first)
+            rc_pass<N, 16, true, false>(tx, ns, buf, src, n_f, live, roots, demod, dst);
+        else if (last)
+            rc_pass<N, 16, false, true>(tx, ns, buf, src, n_f, live, roots, demod, dst);
+        else
+            rc_pass<N, 16, false, false>(tx, ns, buf, src, n_f, live, roots, demod, dst);
+        ns *= 16;
+    }
 }
 
 template <int LOGN>
 int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *roots, const float2 *demod,
               float2 *out, cudaStream_t s) {
-    const size_t smem = 2 * sizeof(float2) * (1u << LOGN);
+    using S = RcShape<LOGN>;
+    const size_t smem = sizeof(float2) * S::NP * S::ROWS;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(range_compress_kernel<LOGN>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int64_t r0 = 0; r0 < n_el; r0 += 2147483647ll) {
-        const int64_t rows = n_el - r0 < 2147483647ll ? n_el - r0 : 2147483647ll;
-        range_compress_kernel<LOGN><<<(unsigned)rows, RC_THREADS, smem, s>>>(
-            cube + r0 * n_f, n_f, roots, demod, out + r0 * ((int64_t)1 << LOGN));
+    const int64_t blocks = (n_el + S::ROWS - 1) / S::ROWS;
+    for (int64_t b0 = 0; b0 < blocks; b0 += 2147483647ll) {
+        const int64_t nb = blocks - b0 < 2147483647ll ? blocks - b0 : 2147483647ll;
+        const int64_t r0 = b0 * S::ROWS;
+        range_compress_kernel<LOGN><<<(unsigned)nb, S::T * S::ROWS, smem, s>>>(
+            cube + r0 * n_f, n_el - r0, n_f, roots, demod, out + r0 * (int64_t)S::N);
     }
     return check_launch("range_compress_kernel");
 }

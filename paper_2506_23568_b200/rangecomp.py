@@ -49,11 +49,11 @@ class RangeProfileSet:
         return (self.t0, self.t0 + (self.n_samples - 1) * self.dt)
 
 
-# The fused single-pass kernel (hhsar_range_compress) is exact to 2e-7 vs the
-# cuFFT path but its radix-4 shared-memory passes are still slower than cuFFT
-# + the demodulation kernel on B200 (config 3: 3.0 vs 2.3 ms), so cuFFT is the
-# default until the register-resident radix-16 version lands.
-_FORCE_CUFFT = os.environ.get("HHSAR_RANGE_FFT", "cufft") != "fused"
+# The fused single-pass kernel (hhsar_range_compress: register radix-16
+# Stockham passes, pad + IDFT + demodulation in one HBM pass) agrees with the
+# cuFFT path to 2e-7 and is 2x faster on B200 (config 3: 1.13 vs 2.28 ms);
+# HHSAR_RANGE_FFT=cufft selects the cuFFT + hhsar_range_demod path.
+_FORCE_CUFFT = os.environ.get("HHSAR_RANGE_FFT", "fused") == "cufft"
 
 
 def profile_axis(freqs, upsample: int):

@@ -66,6 +66,21 @@ def test_range_profiles_vs_reference(hh, small):
     assert prof.t0 == t0 and prof.dt == dt and prof.k_ref == k_ref
 
 
+@pytest.mark.parametrize("upsample", [1, 2, 8, 64, 512])
+def test_fused_range_compression_vs_reference(hh, small, upsample, monkeypatch):
+    """hhsar_range_compress (pad + IDFT + demod in one pass, n_t = 16 ...
+    8192) against numpy's IDFT restatement and, at upsample 8, the
+    reference's own envelopes."""
+    import oracle
+    from paper_2506_23568_b200 import rangecomp
+    monkeypatch.setattr(rangecomp, "_FORCE_CUFFT", False)
+    prof = hh.range_compress(small.cube, upsample)
+    want = oracle.range_compress(small.cube, upsample).envelopes
+    assert rel_l2(prof.envelopes.cpu().numpy(), want) < 2e-6
+    if upsample == 8:
+        assert rel_l2(prof.envelopes.cpu().numpy(), small.z["envelopes"]) < 2e-6
+
+
 def test_backproject_probes_selections_and_empty(hh, small):
     prof = hh.range_compress(small.cube, 8)
     got = hh.backproject(prof, slice(None), small.z["probes"])
