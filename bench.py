@@ -295,9 +295,8 @@ def hhffbpa_leg(index, dev, steps, check=False):
     params = ffbp.FfbpParams(levels=w.levels)
 
     def step():
-        env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
-        return ffbp.hhffbpa_device(env, el, el4, 0.0, dt, k_ref, w.freqs, w.region, w.dims,
-                                   params, w.levels, 2)
+        return ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params,
+                                      w.levels, 2, w.upsample)
 
     for _ in range(3):
         run = step()

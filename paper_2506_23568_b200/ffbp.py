@@ -36,7 +36,7 @@ from .bpa import (ImageVolume, _finish, bpa_volume_device, check_delay_window,
 from .errors import ConfigError, NumericDomainError
 from .model import (C_LIGHT, Subarray, boundary_lattice, leaf_bounds,
                     partition_subarrays, validate_geometry)
-from .rangecomp import RangeProfileSet, range_compress
+from .rangecomp import RangeProfileSet, profile_axis, range_compress, to_device_cube
 from .spectrum import TWO_PI, SubarrayExtents
 
 GRID_PAD = 2  # ffbp.py:32
@@ -184,6 +184,16 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     (multi-GPU subtree ownership).  Unselected grids keep valid = 0 and zero
     counters.
     """
+    pending = plan_lattices(el_dev, sched, region, kgrid, gamma, margin, pad, window_hi, tol,
+                            max_iter)
+    return finish_lattices(pending, newton_grids)
+
+
+def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float, pad: int,
+                  window_hi: float, tol: float = 1e-9, max_iter: int = 50):
+    """Launch the leaf boxes + plan kernels and the asynchronous readback of
+    the descriptors (pinned) on the current stream; returns a pending plan
+    for finish_lattices (which is the only host wait)."""
     import torch
     dev = el_dev.device
     stream = _native.stream_handle()
@@ -199,8 +209,25 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
                  _native.ptr(boundary), bl.shape[0], _native.ptr(geom), _native.ptr(status),
                  stream)
-    host = np.frombuffer(descs_dev.cpu().numpy().tobytes(), dtype=_native.GRID_DTYPE).copy()
-    if int(status.cpu()[0]):
+    host_d = torch.empty(descs_dev.shape, dtype=torch.uint8, pin_memory=True)
+    host_s = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    host_d.copy_(descs_dev, non_blocking=True)
+    host_s.copy_(status, non_blocking=True)
+    done = torch.cuda.Event()
+    done.record()
+    return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom, host_d=host_d,
+                host_s=host_s, done=done, keep=(bounds, leaf_box, boundary, status))
+
+
+def finish_lattices(p, newton_grids=None) -> Lattices:
+    """Wait for the plan, size the pools, launch Newton (current stream)."""
+    import torch
+    p["done"].synchronize()
+    sched, descs_dev, geom = p["sched"], p["descs_dev"], p["geom"]
+    dev = descs_dev.device
+    stream = _native.stream_handle()
+    host = np.frombuffer(p["host_d"].numpy().tobytes(), dtype=_native.GRID_DTYPE).copy()
+    if int(p["host_s"][0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
     dims = host["dims"].astype(np.int64)
     npts = dims.prod(axis=1)
@@ -214,16 +241,24 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     host["col_offset"] = starts
     n_cols = int(cols.sum())
     block_grid = np.searchsorted(starts, np.arange(0, max(n_cols, 1), 128), side="right") - 1
-    descs_dev.copy_(torch.from_numpy(host.view(np.uint8).reshape(-1)), non_blocking=False)
+    # descriptors + Newton block table go up in one pinned, asynchronous copy
+    blob = np.concatenate([host.view(np.uint8).reshape(-1),
+                           block_grid.astype(np.int32).view(np.uint8)])
+    staged = torch.from_numpy(blob).pin_memory()
+    up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
+    up.copy_(staged, non_blocking=True)
+    descs_dev = up[:host.nbytes]
+    bg = up[host.nbytes:]
     total = int(npts.sum())
     positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
     valid = torch.zeros(total, dtype=torch.uint8, device=dev)
     stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
-    bg = torch.as_tensor(block_grid.astype(np.int32), device=dev)
     _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, n_cols,
                  _native.ptr(bg), _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
                  _native.ptr(stats), stream)
-    return Lattices(host, descs_dev, positions, valid, stats, geom)
+    lat = Lattices(host, descs_dev, positions, valid, stats, geom)
+    lat.keep = (staged, up)  # pinned staging must outlive the async copy
+    return lat
 
 
 @dataclass
@@ -248,7 +283,7 @@ class Pipeline:
 
     def __init__(self, env, el_dev, el4, t0: float, dt: float, k_ref: float, kgrid, region,
                  final_dims, params: FfbpParams, levels: int, merge_factor: int = 2,
-                 window_hi=None, newton_grids=None, env_row0: int = 0, sched=None):
+                 window_hi=None, newton_grids=None, env_row0: int = 0, sched=None, lat=None):
         import ctypes
         import torch
         self.dev = env.device
@@ -256,12 +291,12 @@ class Pipeline:
         self.t0, self.dt, self.k_ref = float(t0), float(dt), float(k_ref)
         self.region, self.final_dims, self.params = region, tuple(final_dims), params
         self.kid = _kernel_id(params.kernel)
-        src_pad = GRID_PAD + (3 if params.kernel == "cubic" else 2)  # ffbp.py:468
         if window_hi is None:
             window_hi = t0 + (env.shape[1] - 1) * dt
         self.sched = sched or Schedule(el_dev.shape[0], levels, merge_factor)
-        self.lat = build_lattices(el_dev, self.sched, region, kgrid, params.gamma, params.margin,
-                                  src_pad, window_hi, newton_grids=newton_grids)
+        self.lat = lat or build_lattices(el_dev, self.sched, region, kgrid, params.gamma,
+                                         params.margin, src_pad_of(params), window_hi,
+                                         newton_grids=newton_grids)
         self.values = torch.empty(int(self.lat.npts.sum()), dtype=torch.complex64,
                                   device=self.dev)
         self.lat.values = self.values
@@ -334,6 +369,52 @@ def hhffbpa_device(env, el_dev, el4, t0: float, dt: float, k_ref: float, kgrid, 
                     merge_factor, window_hi).run(vox_range)
 
 
+def src_pad_of(params) -> int:
+    return GRID_PAD + (3 if params.kernel == "cubic" else 2)  # ffbp.py:468
+
+
+_GEO_STREAMS = {}
+
+
+def geometry_stream(device):
+    """Side stream for the data-independent grid construction."""
+    import torch
+    key = torch.device(device).index
+    if key not in _GEO_STREAMS:
+        _GEO_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _GEO_STREAMS[key]
+
+
+def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
+                      levels: int, merge_factor: int = 2, upsample: int = 8,
+                      vox_range=None) -> DeviceRun:
+    """Whole HHFFBPA step from a device cube with the grid construction
+    overlapped with range compression: the lattices depend only on geometry,
+    so plan + Newton run on a side stream while the main stream
+    range-compresses; the leaf stage waits for both."""
+    import torch
+    from .rangecomp import profile_axis, range_compress_device
+    n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
+    window_hi = 0.0 + (n_t - 1) * dt
+    sched = Schedule(el_dev.shape[0], levels, merge_factor)
+    main = torch.cuda.current_stream()
+    geo = geometry_stream(cube_dev.device)
+    geo.wait_stream(main)
+    with torch.cuda.stream(geo):
+        pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
+                                src_pad_of(params), window_hi)
+    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
+    with torch.cuda.stream(geo):
+        lat = finish_lattices(pending)
+    main.wait_stream(geo)
+    # blocks allocated on the side stream are used on the main one from here
+    for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
+        t.record_stream(main)
+    pipe = Pipeline(env, el_dev, el4, 0.0, dt, k_ref, kgrid, region, final_dims, params, levels,
+                    merge_factor, window_hi, sched=sched, lat=lat)
+    return pipe.run(vox_range)
+
+
 def _core_masked(desc, n_valid_core) -> float:
     size = int(np.prod(desc["core_hi"].astype(np.int64) - desc["core_lo"] + 1))
     return 1.0 - (int(n_valid_core) / size)
@@ -398,11 +479,11 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
         final_dims = default_grid_dims(region, kgrid)
     final_dims = tuple(int(d) for d in final_dims)
     levels = params.levels if params.levels is not None else default_levels(cube.aperture)
-    profiles = range_compress(cube, upsample)
-    check_delay_window(profiles, region)
     origin, step = region_grid(region, final_dims)
-    el4 = el_f32x4(profiles.elements_dev)
     if levels == 1:  # ffbp.py:460-464: plain BPA onto the final grid
+        profiles = range_compress(cube, upsample)
+        check_delay_window(profiles, region)
+        el4 = el_f32x4(profiles.elements_dev)
         vol, oow = bpa_volume_device(profiles.envelopes, el4, region, final_dims, profiles.t0,
                                      profiles.dt, profiles.k_ref)
         n = int(np.prod(final_dims))
@@ -411,12 +492,18 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
                 "dims": list(final_dims), "level_points": [[n]], "merge_flags": [],
                 "final_flags": 0, "flagged_fraction": 0.0}
         return _finish(vol, oow, final_dims, origin, step, prov)[0]
+    _native.library()
+    el_dev = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
+                          device="cuda")
+    n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
+    check_delay_window(RangeProfileSet(envelopes=torch.empty((0, n_t)), t0=0.0, dt=dt,
+                                       upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
+                                       freqs=kgrid, elements_dev=el_dev), region)
     if region.z_min <= 0.0:
         raise ConfigError("region must sit strictly in front of the array")
     partition_subarrays(cube.aperture, levels)  # raises ConfigError when too deep
-    run = hhffbpa_device(profiles.envelopes, profiles.elements_dev, el4, profiles.t0,
-                         profiles.dt, profiles.k_ref, kgrid, region, final_dims, params, levels,
-                         merge_factor, window_hi=profiles.window[1])
+    run = hhffbpa_from_cube(to_device_cube(cube.values), el_dev, el_f32x4(el_dev), kgrid,
+                            region, final_dims, params, levels, merge_factor, upsample)
     extra = torch.cat([run.flags, run.lattices.stats.reshape(-1)])
     volume, tail = _finish(run.volume, run.oow, final_dims, origin, step, {}, extra)
     n_flags = run.flags.numel()

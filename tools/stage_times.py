@@ -52,9 +52,8 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
-        run = ffbp.hhffbpa_device(env, el, el4, 0.0, dt, k_ref, w.freqs, w.region, w.dims,
-                                  params, levels, factor)
+        run = ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params, levels,
+                                     factor, w.upsample)
         t1.record()
         torch.cuda.synchronize()
         _native.call = orig_call
