@@ -84,13 +84,15 @@ __device__ __forceinline__ bool llt_exact(const double *ext, const hhsar_geom &g
 // never on the bit-exact lattice-metadata path.  Inputs must lie in the fp32
 // normal range (squared distances of metres: fine).
 __device__ __forceinline__ double rsqrt_d(double a) {
-    const double y = (double)rsqrtf((float)a);
+    double y;  // MUFU.RSQ64H seed (~2^-23), no fp32 round trip
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
     const double e = fma(-(a * y), y, 1.0);
     return fma(0.5 * y, e, y);
 }
 
 __device__ __forceinline__ double rcp_d(double a) {
-    const double y = (double)__frcp_rn((float)a);
+    double y;  // MUFU.RCP64H seed
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
     return fma(y, fma(-a, y, 1.0), y);
 }
 

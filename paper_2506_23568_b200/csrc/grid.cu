@@ -274,113 +274,129 @@ grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__
 }
 
 // ---- Newton columns -------------------------------------------------------------
-__global__ void __launch_bounds__(128)
+// Persistent kernel with PER-LANE work fetching: every lane runs its own
+// (column, plane, iteration) state machine and, when its column is done,
+// grabs the next one from a global counter.  A column's cost varies >10x
+// (failing planes run 50 iterations), so static one-column-per-thread left
+// ~70% of the lanes idle; here lanes stay busy until the work list drains.
+// Work list = the active columns only (desc.act_* rectangle, see
+// grid_plan_kernel): columns outside the near band are masked whatever
+// Newton returns (ffbp.py:294-301) and unreachable ones provably fail, so
+// neither is launched (the caller zeroed `valid`).
+constexpr int NEWTON_THREADS = 128;
+
+__global__ void __launch_bounds__(NEWTON_THREADS)
 grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
                    const int32_t *__restrict__ block_grid, hhsar_geom g,
                    double *__restrict__ positions, uint8_t *__restrict__ valid,
-                   int64_t *__restrict__ stats) {
-    // Work list = the active columns only (desc.act_* rectangle, see
-    // grid_plan_kernel): columns outside the near band are masked whatever
-    // Newton returns (ffbp.py:294-301) and unreachable ones provably fail,
-    // so neither is launched (the caller zeroed `valid`).
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_cols) return;
-    int gi = block_grid[blockIdx.x];
-    while (gi + 1 < n_grids && grids[gi + 1].col_offset <= c) ++gi;
-    const hhsar_grid_desc &D = grids[gi];
-    const int nv = D.dims[1], nn = D.dims[2];
-    const int64_t k = c - D.col_offset;
-    const int wv = D.act_hi[1] - D.act_lo[1] + 1;
-    const int iu = D.act_lo[0] + (int)(k / wv), iv = D.act_lo[1] + (int)(k % wv);
-    const int64_t col = (int64_t)iu * nv + iv;
-    uint8_t *vcol = valid + D.offset + col * nn;
-    double *pcol = positions + 3 * (D.offset + col * nn);
-    unsigned n_pre = 0, core_pre = 0, n_post = 0, core_post = 0, its = 0, solves = 0;
-    const double tu = xadd(D.origin[0], xmul(g.step, (double)iu));
-    const double tv = xadd(D.origin[1], xmul(g.step, (double)iv));
-    const int w_end = D.near_hi[2] + 1;
-    if (w_end > 0) {
-        NewtonGeom G;
-        for (int k = 0; k < 4; ++k) G.ext[k] = D.ext[k];
-        G.gap = box_gap_exact(D.ext);
-        G.c_uv = g.c_uv;
-        G.c_nhi = g.c_nhi;
-        G.c_nlo = g.c_nlo;
-        const bool core_uv = iu >= D.core_lo[0] && iu <= D.core_hi[0] && iv >= D.core_lo[1] &&
-                             iv <= D.core_hi[1];
-        // Flattened march: every lane runs its own (plane, iteration) state, so
-        // a warp costs max over lanes of the TOTAL iterations instead of the
-        // sum over planes of the per-plane maximum.
-        const double max_step2 = g.max_step * g.max_step;
-        double gx = g.center[0], gy = g.center[1], gz = g.center[2];
-        int w = 0, it = 0;
-        double tn = D.origin[2];
-        double x = gx, y = gy, z = gz > g.z_floor ? gz : g.z_floor;
-        while (w < w_end) {
-            ++it;
-            int st = newton_iteration(G, tu, tv, tn, x, y, z, g.tol, max_step2, g.max_step,
-                                      g.z_floor);
-            if (st == 0 && it < g.max_iter) continue;
-            const bool ok = st == 1;
-            its += it;
-            ++solves;
-            uint8_t v = 0;
-            if (w >= D.near_lo[2]) {
-                bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] && y >= D.slack_lo[1] &&
-                           y <= D.slack_hi[1] && z >= D.slack_lo[2] && z <= D.slack_hi[2];
-                bool post = pre;
-                if (pre && D.is_leaf) {
-                    // 2 * max corner distance / c <= window_hi (ffbp.py:320-330)
-                    double dmax = 0.0;
+                   int64_t *__restrict__ stats, unsigned long long *__restrict__ counter) {
+    const double max_step2 = g.max_step * g.max_step;
+    NewtonGeom G;
+    G.c_uv = g.c_uv;
+    G.c_nhi = g.c_nhi;
+    G.c_nlo = g.c_nlo;
+    int gi = -1, acc_gi = -1, w = 0, w_end = 0, it = 0, iu = 0, iv = 0;
+    int64_t base = 0;  // lattice index of plane 0 of the current column
+    bool have = false, core_uv = false;
+    double tu = 0, tv = 0, tn = 0, x = 0, y = 0, z = 0;
+    unsigned acc[6] = {0, 0, 0, 0, 0, 0};
+    auto flush = [&]() {
+        if (acc_gi < 0) return;
+        int64_t *st = stats + (int64_t)acc_gi * HHSAR_GRID_STATS;
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const double cx = (b & 4) ? D.box[3] : D.box[0];
-                        const double cy = (b & 2) ? D.box[4] : D.box[1];
-                        const double cz = (b & 1) ? D.box[5] : D.box[2];
-                        const double d = xsqrt(xadd(xadd(xsq(xsub(x, cx)), xsq(xsub(y, cy))),
-                                                    xsq(xsub(z, cz))));
-                        dmax = fmax(dmax, d);
-                    }
-                    post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
-                }
-                const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
-                n_pre += pre;
-                core_pre += pre && in_core;
-                n_post += post;
-                core_post += post && in_core;
-                v = post;
-                if (pre) {
-                    pcol[3 * w] = x;
-                    pcol[3 * w + 1] = y;
-                    pcol[3 * w + 2] = z;
-                }
-            }
-            vcol[w] = v;
-            if (ok) {
-                gx = x;
-                gy = y;
-                gz = z;
-            } else {
-                gx = g.center[0];
-                gy = g.center[1];
-                gz = g.center[2];
-            }
-            ++w;
-            it = 0;
-            tn = xadd(D.origin[2], xmul(g.step, (double)w));
-            x = gx;
-            y = gy;
-            z = gz > g.z_floor ? gz : g.z_floor;
+        for (int q = 0; q < 6; ++q) {
+            if (acc[q]) atomicAdd((unsigned long long *)(st + q), (unsigned long long)acc[q]);
+            acc[q] = 0;
         }
+    };
+    auto start_plane = [&](const hhsar_grid_desc &D, double sx, double sy, double sz) {
+        tn = xadd(D.origin[2], xmul(g.step, (double)w));
+        x = sx;
+        y = sy;
+        z = sz > g.z_floor ? sz : g.z_floor;
+        it = 0;
+    };
+    while (true) {
+        if (!have) {
+            const unsigned long long c = atomicAdd(counter, 1ull);
+            if (c >= (unsigned long long)n_cols) break;
+            int g2 = block_grid[c >> 7];
+            while (g2 + 1 < n_grids && (unsigned long long)grids[g2 + 1].col_offset <= c) ++g2;
+            if (g2 != acc_gi) {
+                flush();
+                acc_gi = g2;
+            }
+            gi = g2;
+            const hhsar_grid_desc &D = grids[gi];
+            const int64_t k = (int64_t)c - D.col_offset;
+            const int wv = D.act_hi[1] - D.act_lo[1] + 1;
+            iu = D.act_lo[0] + (int)(k / wv);
+            iv = D.act_lo[1] + (int)(k % wv);
+            base = D.offset + ((int64_t)iu * D.dims[1] + iv) * D.dims[2];
+            tu = xadd(D.origin[0], xmul(g.step, (double)iu));
+            tv = xadd(D.origin[1], xmul(g.step, (double)iv));
+            core_uv = iu >= D.core_lo[0] && iu <= D.core_hi[0] && iv >= D.core_lo[1] &&
+                      iv <= D.core_hi[1];
+            w_end = D.near_hi[2] + 1;
+            for (int q = 0; q < 4; ++q) G.ext[q] = D.ext[q];
+            G.gap = box_gap_exact(D.ext);
+            w = 0;
+            have = w_end > 0;
+            if (have) start_plane(D, g.center[0], g.center[1], g.center[2]);
+            continue;
+        }
+        ++it;
+        const int st = newton_iteration(G, tu, tv, tn, x, y, z, g.tol, max_step2, g.max_step,
+                                        g.z_floor);
+        if (st == 0 && it < g.max_iter) continue;
+        // plane w finished: masks, counters, warm start for plane w + 1
+        const hhsar_grid_desc &D = grids[gi];
+        const bool ok = st == 1;
+        acc[4] += it;
+        acc[5] += 1;
+        if (w >= D.near_lo[2]) {
+            const bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] &&
+                             y >= D.slack_lo[1] && y <= D.slack_hi[1] && z >= D.slack_lo[2] &&
+                             z <= D.slack_hi[2];
+            bool post = pre;
+            if (pre && D.is_leaf) {
+                // 2 * max corner distance / c <= window_hi (ffbp.py:320-330)
+                double dmax = 0.0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const double cx = (b & 4) ? D.box[3] : D.box[0];
+                    const double cy = (b & 2) ? D.box[4] : D.box[1];
+                    const double cz = (b & 1) ? D.box[5] : D.box[2];
+                    const double d =
+                        xsqrt(xadd(xadd(xsq(xsub(x, cx)), xsq(xsub(y, cy))), xsq(xsub(z, cz))));
+                    dmax = fmax(dmax, d);
+                }
+                post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
+            }
+            const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
+            acc[0] += pre;
+            acc[1] += pre && in_core;
+            acc[2] += post;
+            acc[3] += post && in_core;
+            if (post) valid[base + w] = 1;
+            if (pre) {
+                double *pp = positions + 3 * (base + w);
+                pp[0] = x;
+                pp[1] = y;
+                pp[2] = z;
+            }
+        }
+        ++w;
+        if (w >= w_end) {
+            have = false;
+            continue;
+        }
+        if (ok)
+            start_plane(D, x, y, z);
+        else
+            start_plane(D, g.center[0], g.center[1], g.center[2]);
     }
-    for (int w = w_end; w < nn; ++w) vcol[w] = 0;
-    int64_t *st = stats + (int64_t)gi * HHSAR_GRID_STATS;
-    if (n_pre) atomicAdd((unsigned long long *)(st + 0), (unsigned long long)n_pre);
-    if (core_pre) atomicAdd((unsigned long long *)(st + 1), (unsigned long long)core_pre);
-    if (n_post) atomicAdd((unsigned long long *)(st + 2), (unsigned long long)n_post);
-    if (core_post) atomicAdd((unsigned long long *)(st + 3), (unsigned long long)core_post);
-    if (its) atomicAdd((unsigned long long *)(st + 4), (unsigned long long)its);
-    if (solves) atomicAdd((unsigned long long *)(st + 5), (unsigned long long)solves);
+    flush();
 }
 
 __global__ void invert_newton_kernel(NewtonGeom G, const double *__restrict__ t,
@@ -435,8 +451,23 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
     HHSAR_REQUIRE(n_cols == 0 || block_grid != nullptr, "grid_newton: block_grid required");
     if (n_cols == 0) return HHSAR_OK;
-    grid_newton_kernel<<<(unsigned)((n_cols + 127) / 128), 128, 0, as_stream(stream)>>>(
-        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats);
+    cudaStream_t s = as_stream(stream);
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_newton_kernel, NEWTON_THREADS,
+                                                      0);
+        if (per_sm <= 0) per_sm = 1;
+    }
+    unsigned long long *counter = nullptr;
+    if (cudaMallocAsync(&counter, sizeof(unsigned long long), s) != cudaSuccess)
+        return set_error(HHSAR_ECUDA, "grid_newton: counter allocation failed");
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
+    int64_t blocks = (int64_t)sm_count() * per_sm;
+    const int64_t need = (n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS;
+    if (blocks > need) blocks = need;
+    grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
+        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter);
+    cudaFreeAsync(counter, s);
     return check_launch("grid_newton_kernel");
 }
 

@@ -66,6 +66,11 @@ def main():
            "lattice_points": int(run.lattices.npts.sum()),
            "valid_points": int(stats[:, 0].sum()),
            "newton_iterations": int(stats[:, 4].sum()),
+           "newton_solves": int(stats[:, 5].sum()),
+           "newton_converged_valid": int(stats[:, 0].sum()),
+           "active_columns": int(np.prod(np.maximum(run.lattices.descs["act_hi"].astype(np.int64)
+                                                    - run.lattices.descs["act_lo"] + 1, 0),
+                                         axis=1).sum()),
            "leaf_units": int(sum(stats[g, 2] * (run.lattices.descs['stop'][g] - run.lattices.descs['start'][g])
                                 for g in range(*run.sched.level_slices[0]))),
            "flags": flags.tolist(), "sim_s": round(t_sim, 2), "runs": res[1:]}
