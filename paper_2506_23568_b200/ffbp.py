@@ -197,26 +197,37 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     import torch
     dev = el_dev.device
     stream = _native.stream_handle()
-    bounds = torch.as_tensor(sched.bounds, dtype=torch.int64, device=dev)
+    bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
+    # one pinned, asynchronous upload: grid descriptors | leaf bounds |
+    # boundary lattice | status word (all 8-byte aligned pieces)
+    parts = [sched.grids.view(np.uint8).reshape(-1), sched.bounds.astype(np.int64).view(np.uint8),
+             bl.view(np.uint8).reshape(-1), np.zeros(8, dtype=np.uint8)]
+    cuts = np.cumsum([0] + [p.size for p in parts])
+    staged = torch.empty(int(cuts[-1]), dtype=torch.uint8, pin_memory=True)
+    sn = staged.numpy()
+    for p, a in zip(parts, cuts[:-1]):
+        sn[a:a + p.size] = p
+    up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
+    up.copy_(staged, non_blocking=True)
+    descs_dev = up[cuts[0]:cuts[1]]
+    bounds = up[cuts[1]:cuts[2]]
+    boundary = up[cuts[2]:cuts[3]]
+    status = up[cuts[3]:cuts[4]]
     leaf_box = torch.empty((sched.n_leaves, 6), dtype=torch.float64, device=dev)
     _native.call("hhsar_leaf_boxes", _native.ptr(el_dev), _native.ptr(bounds), sched.n_leaves,
                  _native.ptr(leaf_box), stream)
-    bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
-    boundary = torch.as_tensor(bl, device=dev)
-    descs_dev = _native.device_struct(sched.grids, dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
     geom = make_geom(region, kgrid, gamma, margin, pad, window_hi, tol, max_iter)
     _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
                  _native.ptr(boundary), bl.shape[0], _native.ptr(geom), _native.ptr(status),
                  stream)
-    host_d = torch.empty(descs_dev.shape, dtype=torch.uint8, pin_memory=True)
-    host_s = torch.empty(1, dtype=torch.int32, pin_memory=True)
-    host_d.copy_(descs_dev, non_blocking=True)
-    host_s.copy_(status, non_blocking=True)
+    back = torch.empty(int(cuts[1]) + 8, dtype=torch.uint8, pin_memory=True)
+    back[:cuts[1]].copy_(descs_dev, non_blocking=True)
+    back[cuts[1]:].copy_(status, non_blocking=True)
     done = torch.cuda.Event()
     done.record()
-    return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom, host_d=host_d,
-                host_s=host_s, done=done, keep=(bounds, leaf_box, boundary, status))
+    return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
+                host_d=back[:cuts[1]], host_s=back[cuts[1]:cuts[1] + 4].view(torch.int32),
+                done=done, keep=(staged, up, leaf_box))
 
 
 def finish_lattices(p, newton_grids=None) -> Lattices:
@@ -377,11 +388,13 @@ _GEO_STREAMS = {}
 
 
 def geometry_stream(device):
-    """Side stream for the data-independent grid construction."""
+    """High-priority side stream for the data-independent grid construction
+    (its small plan kernels must not queue behind the range-compression
+    CTAs: the host waits on them)."""
     import torch
     key = torch.device(device).index
     if key not in _GEO_STREAMS:
-        _GEO_STREAMS[key] = torch.cuda.Stream(device=device)
+        _GEO_STREAMS[key] = torch.cuda.Stream(device=device, priority=-1)
     return _GEO_STREAMS[key]
 
 
@@ -396,14 +409,16 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     from .rangecomp import profile_axis, range_compress_device
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
     window_hi = 0.0 + (n_t - 1) * dt
-    sched = Schedule(el_dev.shape[0], levels, merge_factor)
     main = torch.cuda.current_stream()
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
+    # range compression first: it needs no host preparation and hides the
+    # schedule / plan set-up below
+    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
+    sched = Schedule(el_dev.shape[0], levels, merge_factor)
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)
-    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
     with torch.cuda.stream(geo):
         lat = finish_lattices(pending)
     main.wait_stream(geo)
