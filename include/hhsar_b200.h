@@ -194,9 +194,12 @@ int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_c
  * at values[desc.offset + i] (complex64; masked points get 0).  With
  * downconvert != 0 the stored value is f * exp(-j Phi_leaf(pos)), ready for
  * the next merge (ffbp.py:343-348).  positions/valid/values are the global
- * lattice pools indexed by desc.offset.  el_xyz float32 [N][4].  oow_total
- * accumulates out-of-window point-element delays. */
-int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, const double *positions,
+ * lattice pools indexed by desc.offset; the grids' points occupy the pool
+ * range [point_begin, point_end) and the largest grid has max_grid_points
+ * points (host-known sizes; the kernel compacts the valid points itself).
+ * el_xyz float32 [N][4].  oow_total accumulates out-of-window delays. */
+int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, int64_t point_begin,
+                  int64_t point_end, int64_t max_grid_points, const double *positions,
                   const uint8_t *valid, const float *el_xyz, const void *envelopes,
                   int64_t n_t, double t0, double dt, double k_ref, const hhsar_geom *geom,
                   int downconvert, void *values, int64_t *oow_total, void *stream);

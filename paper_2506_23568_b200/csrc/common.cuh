@@ -278,4 +278,11 @@ __device__ __forceinline__ void warp_add(int64_t *ctr, unsigned v) {
         atomicAdd((unsigned long long *)ctr, (unsigned long long)s);
 }
 
+// leaf2.cu: compacted point-list level-1 backprojection (hhsar_leaf_bp)
+int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t max_points,
+                       int64_t pool_begin, int64_t pool_end, const double *positions,
+                       const uint8_t *valid, const float4 *el, const float2 *env, int64_t n_t,
+                       double t0, double dt, double k_ref, const hhsar_geom &g, int downconvert,
+                       float2 *values, int64_t *oow_total, cudaStream_t s);
+
 }  // namespace hhsar

@@ -205,13 +205,26 @@ __global__ void downconvert_kernel(const hhsar_grid_desc *__restrict__ grids, in
 
 using namespace hhsar;
 
-extern "C" int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, const double *positions,
+extern "C" int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, int64_t point_begin,
+                             int64_t point_end, int64_t max_grid_points, const double *positions,
                              const uint8_t *valid, const float *el_xyz, const void *envelopes,
                              int64_t n_t, double t0, double dt, double k_ref,
                              const hhsar_geom *geom, int downconvert, void *values,
                              int64_t *oow_total, void *stream) {
     HHSAR_REQUIRE(n_grids > 0 && n_grids < (1 << 24) && geom, "leaf_bp: bad grid count");
     HHSAR_REQUIRE(n_t >= 2, "leaf_bp: n_t must be >= 2");
+    HHSAR_REQUIRE(point_begin >= 0 && point_end >= point_begin && point_end < (1ll << 31) &&
+                  max_grid_points >= 0, "leaf_bp: bad point range");
+    static const bool simple = [] {
+        const char *v = getenv("HHSAR_LEAF_KERNEL");
+        return v && v[0] == 's';
+    }();
+    if (!simple)
+        return launch_leaf_points(grids, n_grids, max_grid_points, point_begin, point_end,
+                                  positions, valid, reinterpret_cast<const float4 *>(el_xyz),
+                                  reinterpret_cast<const float2 *>(envelopes), n_t, t0, dt, k_ref,
+                                  *geom, downconvert, reinterpret_cast<float2 *>(values),
+                                  oow_total, as_stream(stream));
     LeafConst k;
     k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
     k.x0 = (float)(t0 / dt);

@@ -324,7 +324,10 @@ class Pipeline:
         if g1 <= g0:
             return
         lat = self.lat
-        _native.call("hhsar_leaf_bp", lat.desc_ptr(g0), g1 - g0, _native.ptr(lat.positions),
+        p_begin = int(lat.descs["offset"][g0])
+        p_end = int(lat.descs["offset"][g1 - 1] + lat.npts[g1 - 1])
+        _native.call("hhsar_leaf_bp", lat.desc_ptr(g0), g1 - g0, p_begin, p_end,
+                     int(lat.npts[g0:g1].max()), _native.ptr(lat.positions),
                      _native.ptr(lat.valid), _native.ptr(self.el4), self.env_ptr,
                      self.env.shape[1], self.t0, self.dt, self.k_ref, _native.ptr(lat.geom), 1,
                      _native.ptr(self.values), _native.ptr(self.oow), _native.stream_handle())
@@ -695,7 +698,8 @@ def level1_reconstruct(profiles: RangeProfileSet, subarray, grid: SubimageGrid) 
     out = torch.empty(flat.shape[0], dtype=torch.complex64, device=dev)
     oow = torch.zeros(1, dtype=torch.int64, device=dev)
     geom = _geom_for(profiles.freqs, 1.0 / float(grid.step[0]))
-    _native.call("hhsar_leaf_bp", _native.ptr(desc_dev), 1, _native.ptr(pos), _native.ptr(val),
+    _native.call("hhsar_leaf_bp", _native.ptr(desc_dev), 1, 0, flat.shape[0], flat.shape[0],
+                 _native.ptr(pos), _native.ptr(val),
                  _native.ptr(el_f32x4(profiles.elements_dev)), _native.ptr(profiles.envelopes),
                  profiles.envelopes.shape[1], float(profiles.t0), float(profiles.dt),
                  float(profiles.k_ref), _native.ptr(geom), 0, _native.ptr(out), _native.ptr(oow),
