@@ -16,7 +16,6 @@
 namespace hhsar {
 
 constexpr int LP_THREADS = 256;
-constexpr int LP_CHUNK = 32;  // elements per staging pass
 constexpr float LP_MAGIC = 12582912.0f;
 constexpr unsigned LP_MAGIC_BITS = 0x4B400000u;
 
@@ -66,6 +65,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
                    const float2 *__restrict__ env, LeafFast k, hhsar_geom g, int downconvert,
                    float2 *__restrict__ values, int64_t *__restrict__ oow_total) {
     static_assert(P % 2 == 0, "points are processed in pairs");
+    constexpr int LP_CHUNK = 2048 / TW;  // elements per staging pass: 32 KB of windows
     __shared__ float4 s_env[LP_CHUNK * TW];
     __shared__ float4 s_el[LP_CHUNK];
     __shared__ int s_lo[LP_CHUNK];
@@ -235,7 +235,7 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
                        const uint8_t *valid, const float4 *el, const float2 *env, int64_t n_t,
                        double t0, double dt, double k_ref, const hhsar_geom &g, int downconvert,
                        float2 *values, int64_t *oow_total, cudaStream_t s) {
-    constexpr int P = 4, TW = 64;
+    constexpr int P = 4;
     LeafFast k;
     k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
     k.x0 = (float)(t0 / dt);
@@ -256,8 +256,21 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
     cudaMemsetAsync(values + pool_begin, 0, (pool_end - pool_begin) * sizeof(float2), s);
     compact_leaf_kernel<<<(unsigned)n_grids, LP_THREADS, 0, s>>>(grids, valid, idx, cnt);
     const int chunks = (int)((max_points + LP_THREADS * P - 1) / (LP_THREADS * P));
-    leaf_points_kernel<P, TW><<<(unsigned)(n_grids * chunks), LP_THREADS, 0, s>>>(
-        grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
+    // window width: a chunk's points span up to the region's depth + lateral
+    // extent; in delay bins that is ~ (region diagonal) / (c dt / 2)
+    const double rd = sqrt(pow(g.region[1] - g.region[0], 2) + pow(g.region[3] - g.region[2], 2) +
+                           pow(g.region[5] - g.region[4], 2));
+    const double bins = 1.25 * rd * 2.0 / (HHSAR_C_LIGHT * dt) + 6.0;  // + pad-shell overhang
+    const unsigned blocks = (unsigned)(n_grids * chunks);
+    if (bins <= 64)
+        leaf_points_kernel<P, 64><<<blocks, LP_THREADS, 0, s>>>(
+            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
+    else if (bins <= 128)
+        leaf_points_kernel<P, 128><<<blocks, LP_THREADS, 0, s>>>(
+            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
+    else
+        leaf_points_kernel<P, 256><<<blocks, LP_THREADS, 0, s>>>(
+            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
     cudaFreeAsync(idx, s);
     cudaFreeAsync(cnt, s);
     return check_launch("leaf_points_kernel");

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--factor", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--random", action="store_true", help="seeded random cube (no Born sim)")
     args = ap.parse_args()
     import torch
     from paper_2506_23568_b200 import _native, bpa, ffbp, rangecomp, workloads
@@ -26,8 +27,14 @@ def main():
     levels = args.levels or w.levels
     factor = args.factor or w.merge_factor
     t = time.perf_counter()
-    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
-                            w.freqs.k_samples)
+    if args.random:
+        # timing and grid statistics are data-independent
+        gen = torch.Generator(device="cuda").manual_seed(w.seed)
+        cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
+                           generator=gen)
+    else:
+        cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                                w.freqs.k_samples)
     torch.cuda.synchronize()
     t_sim = time.perf_counter() - t
     el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
