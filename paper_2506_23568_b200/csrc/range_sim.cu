@@ -138,8 +138,20 @@ __device__ __forceinline__ void rc_pass(int j, int ns, float2 *buf, const float2
     }
     if (!FIRST) {
         const int t = k * (N / (ns * R));  // twiddle exponent step, units of 2 pi / N
+        // w^1, w^2, w^4, w^8 from the float64-accurate table, the other powers
+        // by products (<= 3 roundings): 4 loads instead of R - 1
+        float2 w[R];
+        w[1] = __ldg(roots + t);
+        if (R > 2) w[2] = __ldg(roots + 2 * t);
+        if (R > 4) w[4] = __ldg(roots + 4 * t);
+        if (R > 8) w[8] = __ldg(roots + 8 * t);
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(roots + t * r));
+        for (int r = 3; r < R; ++r) {
+            const int hi = (r & 8) ? 8 : (r & 4) ? 4 : 2;  // highest power-of-two <= r
+            if (r != hi) w[r] = cmul(w[hi], w[r - hi]);
+        }
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
     }
     idft<R>(v);
     if (LAST) {
@@ -170,7 +182,8 @@ struct RcShape {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(RcShape<LOGN>::T * RcShape<LOGN>::ROWS,
+                                  RcShape<LOGN>::T * RcShape<LOGN>::ROWS >= 512 ? 2 : 4)
 range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
                       const float2 *__restrict__ roots, const float2 *__restrict__ demod,
                       float2 *__restrict__ out) {
