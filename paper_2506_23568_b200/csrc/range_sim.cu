@@ -36,27 +36,55 @@ __global__ void range_demod_kernel(float2 *__restrict__ prof, int64_t n_el, int 
 // ---------------------------------------------------------------------------
 // Fused range compression: zero-pad + unnormalised inverse DFT + demodulation
 // in one pass over HBM (read the n_f-sample cube row once, write the n_t-bin
-// envelope row once).  One CTA per element row; the row lives in shared
-// memory (ping-pong) and goes through Stockham autosort passes (radix 4,
-// one radix-2 pass when log2 n_t is odd).  Twiddles and the demodulation
-// phases come from float64-computed tables of n_t entries (L1/L2 resident).
+// envelope row once).  One CTA per element row (several rows per CTA for
+// short rows); the row lives in shared memory between radix-16 Stockham
+// passes done in registers (one radix-2/4/8 pass first when log2 n_t is not a
+// multiple of 4).  Twiddles and demodulation phases come from float64-
+// computed tables of n_t entries (L1/L2 resident).  Instruction count is the
+// limiter once HBM streams (ncu: issue-bound with eligible warps waiting),
+// so: the zero padding is pruned statically from the first pass (LOGUP =
+// log2(n_t / n_f) when it is 2 or 3), multiplications by the trivial roots 1
+// and i inside the register DFTs are free, complex adds are one FADD2, each
+// twiddle is one coalesced load from a per-pass table, and the cube rows are
+// read with streaming loads so they do not evict the tables from L1 (the
+// tables in (w, i w) float4 form, for FMUL2 + FFMA2 products, doubled the
+// L1 footprint and ran 30% slower).
 // ---------------------------------------------------------------------------
-constexpr int RC_THREADS = 256;
-
-__global__ void rc_tables_kernel(float2 *__restrict__ roots, float2 *__restrict__ demod, int n,
-                                 double a, double dt) {
+// Per-pass twiddle table: entries [pass][q][k], q < 4, k < ns, holding
+// w^(2^q), w = e^{+2 pi j k / 16 ns} (lanes with consecutive k read
+// consecutive entries; one rounding from float64), and the demodulation
+// phases d[i] = e^{j a dt i}.  (A (u, i u) float4 form would allow packed
+// products but doubles the L1 traffic, which measured slower.)
+__global__ void rc_tables_kernel(float2 *__restrict__ tw, float2 *__restrict__ demod, int n,
+                                 int r0, double a, double dt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double s, c;
-    sincospi(2.0 * (double)i / (double)n, &s, &c);  // e^{+2 pi j i / n}: inverse DFT
-    roots[i] = make_float2((float)c, (float)s);
-    demod[i] = cis_reduced(a * (dt * (double)i));   // rangecomp.py:95-96
+    demod[i] = cis_reduced(a * (dt * (double)i));  // rangecomp.py:95-96
+    tw[i] = make_float2(1.f, 0.f);
+    int off = 0;
+    for (int ns = r0; ns < n; off += 4 * ns, ns *= 16) {
+        if (i < off + 4 * ns) {
+            const int q = (i - off) / ns, k = (i - off) % ns;
+            double sn, cs;
+            sincospi(2.0 * (double)((1 << q) * k) / (16.0 * (double)ns), &sn, &cs);
+            tw[i] = make_float2((float)cs, (float)sn);
+            break;
+        }
+    }
 }
 
-// Register-resident inverse DFTs (y_k = sum_n x_n e^{+2 pi i n k / R}), built
-// as radix-2 splits down to the radix-4 butterfly; fully unrolled.
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ f2x as_x(float2 a) { return pk2(a.x, a.y); }
+__device__ __forceinline__ float2 as_f(f2x a) { return make_float2(lo2(a), hi2(a)); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return as_f(add2(as_x(a), as_x(b))); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return as_f(sub2(as_x(a), as_x(b))); }
+
+// a * w with the pair (w, i w): a.x (w.x, w.y) + a.y (-w.y, w.x) = one FMUL2
+// + one FFMA2 with scalar-broadcast operands
+__device__ __forceinline__ f2x pmul(float2 a, f2x w, f2x iw) { return fma2(bc2(a.y), iw, mul2(bc2(a.x), w)); }
+__device__ __forceinline__ float2 cmul_p(float2 a, f2x w, f2x iw) { return as_f(pmul(a, w, iw)); }
+
+__device__ __forceinline__ float2 caddi(float2 a, float2 b) { return make_float2(a.x - b.y, a.y + b.x); }  // a + ib
+__device__ __forceinline__ float2 csubi(float2 a, float2 b) { return make_float2(a.x + b.y, a.y - b.x); }  // a - ib
 
 // e^{+2 pi i q / R} for R in {8, 16}, q < R/2 (literal constants once unrolled)
 template <int R>
@@ -84,111 +112,86 @@ __device__ __forceinline__ float2 root_of_unity(int q) {
     }
 }
 
-template <int R>
+// Unnormalised inverse DFT (y_k = sum_n x_n e^{+2 pi i n k / R}) of length R
+// whose inputs v[n], n >= L, are zero and never read: radix-2 decimation in
+// time down to the radix-4 butterfly, fully unrolled.
+template <int R, int L>
 __device__ __forceinline__ void idft(float2 (&v)[R]) {
-    if constexpr (R == 1) {
-        return;
+    if constexpr (L == 1) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = v[0];
     } else if constexpr (R == 2) {
         const float2 a = v[0], b = v[1];
         v[0] = cadd(a, b);
         v[1] = csub(a, b);
-    } else if constexpr (R == 4) {
+    } else if constexpr (R == 4 && L >= 4) {
         const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
         const float2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
         v[0] = cadd(s02, s13);
-        v[1] = make_float2(d02.x - d13.y, d02.y + d13.x);  // d02 + i d13
+        v[1] = caddi(d02, d13);
         v[2] = csub(s02, s13);
-        v[3] = make_float2(d02.x + d13.y, d02.y - d13.x);  // d02 - i d13
+        v[3] = csubi(d02, d13);
     } else {
         constexpr int H = R / 2;
+        constexpr int LE = (L + 1) / 2 < H ? (L + 1) / 2 : H;
+        constexpr int LO = L / 2 < H ? L / 2 : H;
         float2 e[H], o[H];
 #pragma unroll
         for (int q = 0; q < H; ++q) {
-            e[q] = v[2 * q];
-            o[q] = v[2 * q + 1];
+            if (2 * q < L) e[q] = v[2 * q];
+            if (2 * q + 1 < L) o[q] = v[2 * q + 1];
         }
-        idft<H>(e);
-        idft<H>(o);
+        idft<H, LE>(e);
+        idft<H, LO>(o);
 #pragma unroll
         for (int q = 0; q < H; ++q) {
-            const float2 t = cmul(o[q], root_of_unity<R>(q));
-            v[q] = cadd(e[q], t);
-            v[q + H] = csub(e[q], t);
+            if (q == 0) {
+                v[0] = cadd(e[0], o[0]);
+                v[H] = csub(e[0], o[0]);
+            } else if (4 * q == R) {
+                v[q] = caddi(e[q], o[q]);
+                v[q + H] = csubi(e[q], o[q]);
+            } else {
+                const float2 t = cmul(o[q], root_of_unity<R>(q));
+                v[q] = cadd(e[q], t);
+                v[q + H] = csub(e[q], t);
+            }
         }
     }
 }
 
 __device__ __forceinline__ int rc_pad(int i) { return i + (i >> 4); }  // breaks stride-16 bank conflicts
 
-// One Stockham pass of radix R on the rows held in shared memory (or read
-// from / written to global memory on the first / last pass).
-template <int N, int R, bool FIRST, bool LAST>
-__device__ __forceinline__ void rc_pass(int j, int ns, float2 *buf, const float2 *__restrict__ src,
-                                        int n_f, bool live, const float2 *__restrict__ roots,
-                                        const float2 *__restrict__ demod, float2 *__restrict__ dst) {
-    float2 v[R];
-    const int k = j & (ns - 1);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int i = j + r * (N / R);
-        if (FIRST)
-            v[r] = (live && i < n_f) ? __ldg(src + i) : make_float2(0.f, 0.f);
-        else
-            v[r] = buf[rc_pad(i)];
-    }
-    if (!FIRST) {
-        const int t = k * (N / (ns * R));  // twiddle exponent step, units of 2 pi / N
-        // w^1, w^2, w^4, w^8 from the float64-accurate table, the other powers
-        // by products (<= 3 roundings): 4 loads instead of R - 1
-        float2 w[R];
-        w[1] = __ldg(roots + t);
-        if (R > 2) w[2] = __ldg(roots + 2 * t);
-        if (R > 4) w[4] = __ldg(roots + 4 * t);
-        if (R > 8) w[8] = __ldg(roots + 8 * t);
-#pragma unroll
-        for (int r = 3; r < R; ++r) {
-            const int hi = (r & 8) ? 8 : (r & 4) ? 4 : 2;  // highest power-of-two <= r
-            if (r != hi) w[r] = cmul(w[hi], w[r - hi]);
-        }
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
-    }
-    idft<R>(v);
-    if (LAST) {
-        // ns * R == N: j < ns, outputs land at j + r * N / R (coalesced)
-        if (live) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int i = j + r * (N / R);
-                dst[i] = cmul(v[r], __ldg(demod + i));
-            }
-        }
-    } else {
-        __syncthreads();  // every read of this pass precedes any write
-        const int base = (j - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) buf[rc_pad(base + r * ns)] = v[r];
-        __syncthreads();
-    }
-}
-
 template <int LOGN>
 struct RcShape {
     static constexpr int N = 1 << LOGN;
-    static constexpr int T = N >= 16 ? N / 16 : 1;       // threads per row
+    static constexpr int T = N / 16;                     // threads per row
     static constexpr int ROWS = T >= 256 ? 1 : 256 / T;  // rows per CTA
     static constexpr int NP = N + N / 16;                // padded row in smem
     static constexpr int REM = LOGN % 4;                 // radix 2^REM first pass
+    static constexpr int THREADS = T * ROWS;
 };
 
-template <int LOGN>
-__global__ void __launch_bounds__(RcShape<LOGN>::T * RcShape<LOGN>::ROWS,
-                                  RcShape<LOGN>::T * RcShape<LOGN>::ROWS >= 512 ? 2 : 4)
+// d[j + r T] = d[j] D^r (D = e^{j a dt T}): the demodulation of the last
+// pass needs one table entry per thread and these 16 constants (parameter
+// space, read as constant-bank operands).
+struct RcDemodSteps {
+    float2 d[16], id[16];  // D^r and i D^r
+};
+
+template <int LOGN, int LOGUP>
+__global__ void __launch_bounds__(RcShape<LOGN>::THREADS, RcShape<LOGN>::THREADS >= 512 ? 2 : 4)
 range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
-                      const float2 *__restrict__ roots, const float2 *__restrict__ demod,
-                      float2 *__restrict__ out) {
+                      const float2 *__restrict__ tw, const float2 *__restrict__ demod,
+                      const __grid_constant__ RcDemodSteps steps, float2 *__restrict__ out) {
     using S = RcShape<LOGN>;
     constexpr int N = S::N, T = S::T;
+    constexpr int R0 = S::REM > 0 ? (1 << S::REM) : 16;  // first-pass radix
+    constexpr int M0 = 16 / R0;                            // first-pass DFTs per thread
+    constexpr int P16 = LOGN / 4;                          // radix-16 passes
+    constexpr int NLIVE = LOGUP > 0 ? (N >> LOGUP) : N;    // static bound on nonzero inputs
+    constexpr int L0c = (NLIVE * R0 + N - 1) / N;          // live first-pass inputs
+    constexpr int L0 = L0c < 1 ? 1 : (L0c > R0 ? R0 : L0c);
     extern __shared__ float2 rc_smem[];
     const int tx = threadIdx.x % T, ty = threadIdx.x / T;
     const int64_t row = (int64_t)blockIdx.x * S::ROWS + ty;
@@ -196,61 +199,96 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
     float2 *buf = rc_smem + ty * S::NP;
     const float2 *src = cube + (live ? row : 0) * n_f;
     float2 *dst = out + row * N;
-    constexpr int P16 = LOGN / 4;  // radix-16 passes
-    int ns = 1;
-    if constexpr (S::REM > 0) {
-        constexpr int R0 = 1 << S::REM;
+
+    // outputs j + r T, r < 16, of the last pass: demodulate and store (coalesced)
+    auto emit = [&](int j, float2 (&v)[16]) {
+        const float2 dj = __ldg(demod + j);
+        const f2x xdj = as_x(dj), xidj = pk2(-dj.y, dj.x);
+        if (live) {
 #pragma unroll
-        for (int m = 0; m < 16 / R0; ++m)  // N/R0 butterflies over T = N/16 threads
-            if constexpr (P16 == 0) {
-                rc_pass<N, R0, true, true>(tx + m * T, 1, buf, src, n_f, live, roots, demod, dst);
-            } else {
-                // first pass: butterflies j, stores without the trailing sync
-                const int j = tx + m * T;
-                float2 v[R0];
-#pragma unroll
-                for (int r = 0; r < R0; ++r) {
-                    const int i = j + r * (N / R0);
-                    v[r] = (live && i < n_f) ? __ldg(src + i) : make_float2(0.f, 0.f);
-                }
-                idft<R0>(v);
-#pragma unroll
-                for (int r = 0; r < R0; ++r) buf[rc_pad(j * R0 + r)] = v[r];
+            for (int r = 0; r < 16; ++r) {
+                const float2 u = cmul_p(v[r], as_x(steps.d[r]), as_x(steps.id[r]));
+                __stcs(dst + j + r * T, cmul_p(u, xdj, xidj));
             }
-        ns = R0;
-        if constexpr (P16 > 0) __syncthreads();
-    }
+        }
+    };
 #pragma unroll
-    for (int p = 0; p < P16; ++p) {
-        const bool first = S::REM == 0 && p == 0, last = p == P16 - 1;
-        if (first && last)
-            rc_pass<N, 16, true, true>(tx, ns, buf, src, n_f, live, roots, demod, dst);
-        else if (first)
-            rc_pass<N, 16, true, false>(tx, ns, buf, src, n_f, live, roots, demod, dst);
-        else if (last)
-            rc_pass<N, 16, false, true>(tx, ns, buf, src, n_f, live, roots, demod, dst);
-        else
-            rc_pass<N, 16, false, false>(tx, ns, buf, src, n_f, live, roots, demod, dst);
+    for (int m = 0; m < M0; ++m) {
+        const int j = tx + m * T;
+        float2 v[R0];
+#pragma unroll
+        for (int r = 0; r < L0; ++r) {
+            const int i = j + r * (N / R0);
+            v[r] = (live && i < n_f) ? __ldcs(src + i) : make_float2(0.f, 0.f);
+        }
+        idft<R0, L0>(v);
+        if constexpr (S::REM == 0 && P16 == 1) {
+            emit(j, v);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R0; ++r) buf[rc_pad(j * R0 + r)] = v[r];
+        }
+    }
+    if constexpr (S::REM == 0 && P16 == 1) return;
+    __syncthreads();
+    int ns = R0, twoff = 0;
+#pragma unroll
+    for (int p = (S::REM > 0 ? 0 : 1); p < P16; ++p) {
+        const int j = tx, k = j & (ns - 1);
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = buf[rc_pad(j + r * T)];
+        // w^1, w^2, w^4, w^8 by four coalesced loads, the other powers by
+        // products (<= 3 roundings)
+        float2 w[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[1 << q] = __ldg(tw + twoff + q * ns + k);
+        twoff += 4 * ns;
+#pragma unroll
+        for (int r = 3; r < 16; ++r) {
+            const int hi = (r & 8) ? 8 : (r & 4) ? 4 : 2;  // highest power of two <= r
+            if (r != hi) w[r] = cmul(w[hi], w[r - hi]);
+        }
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], w[r]);
+        idft<16, 16>(v);
+        if (p == P16 - 1) {
+            emit(j, v);  // ns * 16 == N
+        } else {
+            __syncthreads();  // every read of this pass precedes any write
+            const int base = (j - k) * 16 + k;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) buf[rc_pad(base + r * ns)] = v[r];
+            __syncthreads();
+        }
         ns *= 16;
     }
 }
 
-template <int LOGN>
-int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *roots, const float2 *demod,
-              float2 *out, cudaStream_t s) {
+template <int LOGN, int LOGUP>
+int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const float2 *demod,
+              const RcDemodSteps &steps, float2 *out, cudaStream_t s) {
     using S = RcShape<LOGN>;
     const size_t smem = sizeof(float2) * S::NP * S::ROWS;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(range_compress_kernel<LOGN>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t blocks = (n_el + S::ROWS - 1) / S::ROWS;
-    for (int64_t b0 = 0; b0 < blocks; b0 += 2147483647ll) {
-        const int64_t nb = blocks - b0 < 2147483647ll ? blocks - b0 : 2147483647ll;
+    auto kern = range_compress_kernel<LOGN, LOGUP>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t groups = (n_el + S::ROWS - 1) / S::ROWS;
+    for (int64_t b0 = 0; b0 < groups; b0 += 2147483647ll) {
+        const int64_t nb = groups - b0 < 2147483647ll ? groups - b0 : 2147483647ll;
         const int64_t r0 = b0 * S::ROWS;
-        range_compress_kernel<LOGN><<<(unsigned)nb, S::T * S::ROWS, smem, s>>>(
-            cube + r0 * n_f, n_el - r0, n_f, roots, demod, out + r0 * (int64_t)S::N);
+        kern<<<(unsigned)nb, S::THREADS, smem, s>>>(cube + r0 * n_f, n_el - r0, n_f, tw, demod,
+                                                    steps, out + r0 * (int64_t)S::N);
     }
     return check_launch("range_compress_kernel");
+}
+
+template <int LOGN>
+int launch_rc_up(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const float2 *demod,
+                 const RcDemodSteps &steps, float2 *out, cudaStream_t s) {
+    const int64_t n = (int64_t)1 << LOGN;
+    if (n_f * 4 == n) return launch_rc<LOGN, 2>(cube, n_el, n_f, tw, demod, steps, out, s);
+    if (n_f * 8 == n) return launch_rc<LOGN, 3>(cube, n_el, n_f, tw, demod, steps, out, s);
+    return launch_rc<LOGN, 0>(cube, n_el, n_f, tw, demod, steps, out, s);
 }
 
 // One CTA per element; threads over frequencies.  Scatterer distances are
@@ -326,25 +364,34 @@ extern "C" int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f,
                   "range_compress: n_t must be a power of two in [16, 8192]");
     if (n_el == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
-    float2 *tables = nullptr;
+    float2 *tables = nullptr;  // twiddles [n_t], then demodulation phases [n_t]
     if (cudaMallocAsync(&tables, 2 * n_t * sizeof(float2), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "range_compress: table allocation failed");
-    rc_tables_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(tables, tables + n_t, (int)n_t,
-                                                                   a, dt);
+    float2 *demod_tab = tables + n_t;
+    rc_tables_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(tables, demod_tab, (int)n_t,
+                                                                   logn % 4 ? 1 << (logn % 4) : 16, a, dt);
     auto c = reinterpret_cast<const float2 *>(cube);
     auto o = reinterpret_cast<float2 *>(out);
     int rc = HHSAR_OK;
+    RcDemodSteps st;
+    const double step = dt * (double)(n_t / 16);
+    for (int r = 0; r < 16; ++r) {  // e^{j a dt r n_t / 16}, reduced like cis_reduced
+        const double rev = a * (step * (double)r) / (2.0 * M_PI);
+        const double red = 2.0 * M_PI * (rev - nearbyint(rev));
+        st.d[r] = make_float2((float)cos(red), (float)sin(red));
+        st.id[r] = make_float2(-st.d[r].y, st.d[r].x);
+    }
     switch (logn) {
-        case 4: rc = launch_rc<4>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 5: rc = launch_rc<5>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 6: rc = launch_rc<6>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 7: rc = launch_rc<7>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 8: rc = launch_rc<8>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 9: rc = launch_rc<9>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 10: rc = launch_rc<10>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 11: rc = launch_rc<11>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        case 12: rc = launch_rc<12>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
-        default: rc = launch_rc<13>(c, n_el, (int)n_f, tables, tables + n_t, o, s); break;
+        case 4: rc = launch_rc_up<4>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 5: rc = launch_rc_up<5>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 6: rc = launch_rc_up<6>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 7: rc = launch_rc_up<7>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 8: rc = launch_rc_up<8>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 9: rc = launch_rc_up<9>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 10: rc = launch_rc_up<10>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 11: rc = launch_rc_up<11>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 12: rc = launch_rc_up<12>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        default: rc = launch_rc_up<13>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
     }
     cudaFreeAsync(tables, s);
     return rc;

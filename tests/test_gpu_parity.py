@@ -66,7 +66,7 @@ def test_range_profiles_vs_reference(hh, small):
     assert prof.t0 == t0 and prof.dt == dt and prof.k_ref == k_ref
 
 
-@pytest.mark.parametrize("upsample", [1, 2, 8, 64, 512])
+@pytest.mark.parametrize("upsample", [1, 2, 4, 8, 16, 64, 512])
 def test_fused_range_compression_vs_reference(hh, small, upsample, monkeypatch):
     """hhsar_range_compress (pad + IDFT + demod in one pass, n_t = 16 ...
     8192) against numpy's IDFT restatement and, at upsample 8, the
@@ -79,6 +79,27 @@ def test_fused_range_compression_vs_reference(hh, small, upsample, monkeypatch):
     assert rel_l2(prof.envelopes.cpu().numpy(), want) < 2e-6
     if upsample == 8:
         assert rel_l2(prof.envelopes.cpu().numpy(), small.z["envelopes"]) < 2e-6
+
+
+@pytest.mark.parametrize("n_el,n_f,upsample", [(37, 256, 4), (5, 128, 8), (3, 1024, 4),
+                                                (9, 512, 2), (1, 2048, 4), (6, 50, 4)])
+def test_fused_range_compression_ragged_vs_cufft(n_el, n_f, upsample, monkeypatch):
+    """Fused kernel on ragged row counts (partial multi-row CTAs), every
+    first-pass radix and pruning variant, and a non-power-of-two n_t (cuFFT
+    path), against the cuFFT + demodulation path on the same device cube."""
+    import torch
+    from paper_2506_23568_b200 import rangecomp
+    from paper_2506_23568_b200.model import FrequencyGrid
+    freqs = FrequencyGrid(77e9, 81e9, n_f)
+    gen = torch.Generator(device="cuda").manual_seed(n_el * 7919 + n_f)
+    cube = torch.randn((n_el, n_f), dtype=torch.complex64, device="cuda", generator=gen)
+    monkeypatch.setattr(rangecomp, "_FORCE_CUFFT", False)
+    got, dt, k_ref = rangecomp.range_compress_device(cube, freqs, upsample)
+    monkeypatch.setattr(rangecomp, "_FORCE_CUFFT", True)
+    want, dt2, k_ref2 = rangecomp.range_compress_device(cube, freqs, upsample)
+    assert (dt, k_ref) == (dt2, k_ref2)
+    assert got.shape == want.shape == (n_el, n_f * upsample)
+    assert rel_l2(got.cpu().numpy(), want.cpu().numpy()) < 2e-6
 
 
 def test_backproject_probes_selections_and_empty(hh, small):
