@@ -209,14 +209,14 @@ __device__ __forceinline__ void keys_weights(float f, float w[4]) {
 // Lattice interpolation with the reference's hull rules (_kernels.py:117-189):
 // linear needs every coordinate in [0, n-1] (base clamped to n-2), cubic in
 // [1, n-2] (base clamped to n-3); outside -> ok = false, value 0.
-// vals is [nu][nv][nn] complex64.
-template <int KERNEL>
+// vals is [nu][nv][nn] complex64.  TU: type of the u, v coordinates (double
+// on the API path, float inside the merge kernels); n is always double.
+template <int KERNEL, typename TU = double>
 __device__ __forceinline__ bool lattice_sample(const float2 *__restrict__ vals, int nu, int nv,
-                                               int nn, double cu, double cv, double cn,
-                                               float2 &out) {
+                                               int nn, TU cu, TU cv, double cn, float2 &out) {
     out = make_float2(0.f, 0.f);
     if (KERNEL == 0) {
-        if (!(cu >= 0.0 && cu <= nu - 1 && cv >= 0.0 && cv <= nv - 1 && cn >= 0.0 &&
+        if (!(cu >= TU(0) && cu <= TU(nu - 1) && cv >= TU(0) && cv <= TU(nv - 1) && cn >= 0.0 &&
               cn <= nn - 1))
             return false;
         int iu = min((int)cu, nu - 2), iv = min((int)cv, nv - 2), iw = min((int)cn, nn - 2);
@@ -240,7 +240,7 @@ __device__ __forceinline__ bool lattice_sample(const float2 *__restrict__ vals, 
         out = acc;
         return true;
     } else {
-        if (!(cu >= 1.0 && cu <= nu - 2 && cv >= 1.0 && cv <= nv - 2 && cn >= 1.0 &&
+        if (!(cu >= TU(1) && cu <= TU(nu - 2) && cv >= TU(1) && cv <= TU(nv - 2) && cn >= 1.0 &&
               cn <= nn - 2))
             return false;
         int iu = min((int)cu, nu - 3), iv = min((int)cv, nv - 3), iw = min((int)cn, nn - 3);

@@ -99,25 +99,187 @@ leaf_bp_kernel(const hhsar_grid_desc *__restrict__ grids, int slices,
     if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
 }
 
+// ---- merge stages -----------------------------------------------------------
+// Per-child constants of one merge launch, prepared once (merge_prep_kernel)
+// so the per-point loop reads them instead of re-deriving them (and pays no
+// float64 -> float32 conversions on the XU pipe per point and child).
+struct __align__(16) MergeChild {
+    double ext[4];   // lateral element bbox
+    double o_n;      // lattice origin along n
+    double gap;      // 4 dx^2 + 4 dy^2 (spectrum.py:142-144)
+    int64_t offset;  // first lattice point in the value pool
+    int32_t nu, nv, nn, pad_;
+    float ef[4];     // ext as float32
+    float ku, kv;    // c_uv * width / step (u, v lattice units per unit of the float form)
+    float ou, ov;    // -origin_{u,v} / step
+    float hu, hv;    // largest interpolation base along u, v (n - 2 linear, n - 3 cubic)
+};
+
+__global__ void merge_prep_kernel(const hhsar_grid_desc *__restrict__ d, int n, hhsar_geom g,
+                                  int kernel, MergeChild *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const hhsar_grid_desc &D = d[i];
+    MergeChild c;
+    const double inv_step = 1.0 / g.step;
+    for (int k = 0; k < 4; ++k) {
+        c.ext[k] = D.ext[k];
+        c.ef[k] = (float)D.ext[k];
+    }
+    const double wx = D.ext[1] - D.ext[0], wy = D.ext[3] - D.ext[2];
+    c.o_n = D.origin[2];
+    c.gap = 4.0 * (wx * wx) + 4.0 * (wy * wy);
+    c.offset = D.offset;
+    c.nu = D.dims[0];
+    c.nv = D.dims[1];
+    c.nn = D.dims[2];
+    c.pad_ = 0;
+    c.ku = (float)(g.c_uv * wx * inv_step);
+    c.kv = (float)(g.c_uv * wy * inv_step);
+    c.ou = (float)(-D.origin[0] * inv_step);
+    c.ov = (float)(-D.origin[1] * inv_step);
+    c.hu = (float)(D.dims[0] - (kernel ? 3 : 2));
+    c.hv = (float)(D.dims[1] - (kernel ? 3 : 2));
+    out[i] = c;
+}
+
+// 7 x 16-B loads (the struct is 112 B, 16-B aligned)
+__device__ __forceinline__ MergeChild load_child(const MergeChild *p) {
+    static_assert(sizeof(MergeChild) == 112, "MergeChild layout");
+    MergeChild c;
+    const uint4 *src = reinterpret_cast<const uint4 *>(p);
+    uint4 *dst = reinterpret_cast<uint4 *>(&c);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) dst[k] = __ldg(src + k);
+    return c;
+}
+
+// floor(c) for 0 <= c < 2^22 without F2I/I2F (XU pipe): round-down add of
+// 1.5 * 2^23 leaves the integer in the low mantissa bits.  Base clamped to hi.
+__device__ __forceinline__ void split_f(float c, float hi, int &i, float &f) {
+    const float magic = 12582912.0f;
+    float b = __fadd_rd(c, magic) - magic;
+    b = fminf(b, hi);
+    i = __float_as_int(b + magic) - __float_as_int(magic);
+    f = c - b;
+}
+__device__ __forceinline__ void split_d(double c, int hi, int &i, float &f) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dadd_rd(c, magic);
+    i = min(__double2loint(t), hi);
+    f = (float)(c - (double)i);
+}
+
+// Lattice interpolation with the reference's hull rules (_kernels.py:117-189)
+// on float u, v and double n lattice coordinates.
 template <int KERNEL>
-__device__ __forceinline__ bool merge_point(const hhsar_grid_desc *__restrict__ kids, int nk,
+__device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, const MergeChild &C,
+                                             float cu, float cv, double cn, float2 &out) {
+    out = make_float2(0.f, 0.f);
+    const int lo = KERNEL ? 1 : 0;
+    if (!(cu >= (float)lo && cu <= C.hu + 1.f && cv >= (float)lo && cv <= C.hv + 1.f &&
+          cn >= (double)lo && cn <= (double)(C.nn - 1 - lo)))
+        return false;
+    int iu, iv, iw;
+    float fu, fv, fn;
+    split_f(cu, C.hu, iu, fu);
+    split_f(cv, C.hv, iv, fv);
+    split_d(cn, C.nn - (KERNEL ? 3 : 2), iw, fn);
+    const int su = C.nv * C.nn;  // lattices hold < 2^31 points (int32 dims product)
+    const float2 *base = vals + C.offset;
+    float2 acc = make_float2(0.f, 0.f);
+    if (KERNEL == 0) {
+        const float2 *b = base + ((iu * C.nv + iv) * C.nn + iw);
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const float wa = a ? fu : 1.f - fu;
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb) {
+                const float wb = bb ? fv : 1.f - fv;
+                const float2 *row = b + a * su + bb * C.nn;
+                const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
+                const float w0 = wa * wb * (1.f - fn), w1 = wa * wb * fn;
+                acc.x = fmaf(v0.x, w0, fmaf(v1.x, w1, acc.x));
+                acc.y = fmaf(v0.y, w0, fmaf(v1.y, w1, acc.y));
+            }
+        }
+    } else {
+        float wu[4], wv[4], wn[4];
+        keys_weights(fu, wu);
+        keys_weights(fv, wv);
+        keys_weights(fn, wn);
+        const float2 *b = base + (((iu - 1) * C.nv + (iv - 1)) * C.nn + (iw - 1));
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const float2 *row = b + a * su + bb * C.nn;
+                const float w = wu[a] * wv[bb];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float2 v = __ldg(row + c);
+                    acc.x = fmaf(v.x, w * wn[c], acc.x);
+                    acc.y = fmaf(v.y, w * wn[c], acc.y);
+                }
+            }
+    }
+    out = acc;
+    return true;
+}
+
+__device__ __forceinline__ float sqrt_fast(float a) { return a * rsqrtf(fmaxf(a, 1e-30f)); }
+
+// exp(j phi), float64 phase of any size: reduction by 2 pi with a magic-number
+// round (no FRND), then the fp32 SFU sincos.
+__device__ __forceinline__ float2 cis_fast(double phi) {
+    const double magic = 6755399441055744.0;
+    const double n = fma(phi, 0.15915494309189535, magic) - magic;
+    float s, c;
+    __sincosf((float)fma(-6.283185307179586, n, phi), &s, &c);
+    return make_float2(c, s);
+}
+
+// Sum over children of interp_child(llt_child(p)) exp(j (Phi_child(p) -
+// phi_parent)) at point p (ffbp.py:378-412).  Mixed precision, by what each
+// quantity feeds:
+// * u, v in float32 via d_a - d_b = (e1 - e0)(a_x + b_x) / (d_a + d_b): no
+//   cancellation; absolute error ~1e-7 m in (a_x + b_x), i.e. < 1e-5 lattice
+//   steps;
+// * the four corner distances, r, sqrt(r^2 - gap), n and the phase in float64
+//   (SFU-seeded rsqrt + one Newton step, 1e-13): the phase is ~1e3 rad and a
+//   float32 distance would cost ~1e-4 rad per level;
+// * lattice coordinates by multiplication with 1/step, floors by magic-number
+//   adds (no float64 division, no F2I/I2F).
+template <int KERNEL>
+__device__ __forceinline__ bool merge_point(const MergeChild *__restrict__ kids, int nk,
                                             const float2 *__restrict__ kv, const hhsar_geom &g,
-                                            double x, double y, double z, double phi_parent,
-                                            float2 &acc) {
+                                            double inv_step, double x, double y, double z,
+                                            double phi_parent, float2 &acc) {
     acc = make_float2(0.f, 0.f);
     bool good = true;
+    const float xf = (float)x, yf = (float)y;
+    const double z2 = z * z;
+    const float z2f = (float)z2;
     for (int c = 0; c < nk; ++c) {
-        const hhsar_grid_desc &C = kids[c];
-        const double gap = box_gap_exact(C.ext);
-        const LltPhase L = llt_phase(C.ext, gap, g.c_uv, g.c_nhi, g.c_nlo, g.k_min, g.k_max, x, y, z);
-        const double cu = (L.u - C.origin[0]) / g.step;
-        const double cv = (L.v - C.origin[1]) / g.step;
-        const double cn = (L.n - C.origin[2]) / g.step;
+        const MergeChild C = load_child(kids + c);
+        const float axf = xf - C.ef[0], bxf = xf - C.ef[1], ayf = yf - C.ef[2], byf = yf - C.ef[3];
+        const float dx0 = axf < 0.f ? axf : (bxf > 0.f ? bxf : 0.f);  // x - clip(x, e0, e1)
+        const float dy0 = ayf < 0.f ? ayf : (byf > 0.f ? byf : 0.f);
+        const float dyz = fmaf(dy0, dy0, z2f), dxz = fmaf(dx0, dx0, z2f);
+        const float da = sqrt_fast(fmaf(axf, axf, dyz)), db = sqrt_fast(fmaf(bxf, bxf, dyz));
+        const float dc = sqrt_fast(fmaf(ayf, ayf, dxz)), dd = sqrt_fast(fmaf(byf, byf, dxz));
+        const float cu = __fdividef(C.ku * (axf + bxf), da + db) + C.ou;
+        const float cv = __fdividef(C.kv * (ayf + byf), dc + dd) + C.ov;
+        const double ax = x - C.ext[0], bx = x - C.ext[1], ay = y - C.ext[2], by = y - C.ext[3];
+        const double xa = ax * ax, xb = bx * bx, ya = ay * ay, yb = by * by;
+        const double r = ((sqrt_d(xa + ya + z2) + sqrt_d(xa + yb + z2)) + sqrt_d(xb + ya + z2)) +
+                         sqrt_d(xb + yb + z2);
+        const double sq = sqrt_d(fma(r, r, -C.gap));
+        const double cn = (fma(g.c_nhi, sq, -g.c_nlo * r) - C.o_n) * inv_step;
         float2 s;
-        const bool ok = lattice_sample<KERNEL>(kv + C.offset, C.dims[0], C.dims[1], C.dims[2], cu,
-                                               cv, cn, s);
+        const bool ok = sample_child<KERNEL>(kv, C, cu, cv, cn, s);
         good &= ok;
-        if (ok) cfma(acc, s, cis_reduced(L.phi - phi_parent));
+        if (ok) cfma(acc, s, cis_fast(fma(0.25 * g.k_max, sq, 0.25 * g.k_min * r) - phi_parent));
     }
     if (!good) acc = make_float2(0.f, 0.f);
     return good;
@@ -127,7 +289,7 @@ template <int KERNEL>
 __global__ void __launch_bounds__(MERGE_THREADS)
 merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, int64_t n_points,
                    const double *__restrict__ positions, const uint8_t *__restrict__ valid,
-                   const hhsar_grid_desc *__restrict__ kids, int fanout,
+                   const MergeChild *__restrict__ kids, int fanout,
                    const float2 *__restrict__ kv, hhsar_geom g, int downconvert,
                    float2 *__restrict__ out, int64_t *__restrict__ flagged) {
     const int64_t base = parents[0].offset;
@@ -142,7 +304,8 @@ merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, i
             downconvert ? sdc_phase_fast(P.ext, box_gap_exact(P.ext), g.k_min, g.k_max, x, y, z)
                         : 0.0;
         float2 acc;
-        fl = !merge_point<KERNEL>(kids + (int64_t)p * fanout, fanout, kv, g, x, y, z, phi_p, acc);
+        fl = !merge_point<KERNEL>(kids + (int64_t)p * fanout, fanout, kv, g, rcp_d(g.step), x, y,
+                                  z, phi_p, acc);
         out[i] = acc;
     } else {
         out[i] = make_float2(0.f, 0.f);
@@ -154,20 +317,39 @@ template <int KERNEL>
 __global__ void __launch_bounds__(MERGE_THREADS)
 merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx,
                        int ny, int nz, int64_t vb, int64_t ve,
-                       const hhsar_grid_desc *__restrict__ kids, int nk,
+                       const MergeChild *__restrict__ kids, int nk,
                        const float2 *__restrict__ kv, hhsar_geom g, float2 *__restrict__ out,
                        int64_t *__restrict__ flagged) {
     const int64_t v = vb + (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
     if (v >= ve) return;
-    const int iz = (int)(v % nz), iy = (int)((v / nz) % ny), ix = (int)(v / ((int64_t)nz * ny));
+    int ix, iy, iz;
+    if (ve <= 0x7fffffff) {  // 32-bit index arithmetic (every BASELINE config)
+        const unsigned u = (unsigned)v, t = u / (unsigned)nz;
+        iz = (int)(u - t * (unsigned)nz);
+        iy = (int)(t % (unsigned)ny);
+        ix = (int)(t / (unsigned)ny);
+    } else {
+        iz = (int)(v % nz);
+        iy = (int)((v / nz) % ny);
+        ix = (int)(v / ((int64_t)nz * ny));
+    }
     (void)nx;
     const double x = __dadd_rn(ox, __dmul_rn(sx, (double)ix));
     const double y = __dadd_rn(oy, __dmul_rn(sy, (double)iy));
     const double z = __dadd_rn(oz, __dmul_rn(sz, (double)iz));
     float2 acc;
-    const unsigned fl = !merge_point<KERNEL>(kids, nk, kv, g, x, y, z, 0.0, acc);
+    const unsigned fl = !merge_point<KERNEL>(kids, nk, kv, g, rcp_d(g.step), x, y, z, 0.0, acc);
     out[v - vb] = acc;
     warp_add(flagged, fl);
+}
+
+// Per-child constants for a merge launch (stream-ordered scratch).
+static int prep_children(const hhsar_grid_desc *kids, int64_t n, const hhsar_geom &g, int kernel,
+                         MergeChild **out, cudaStream_t s) {
+    if (cudaMallocAsync(out, n * sizeof(MergeChild), s) != cudaSuccess)
+        return set_error(HHSAR_ECUDA, "merge: scratch allocation failed");
+    merge_prep_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(kids, (int)n, g, kernel, *out);
+    return check_launch("merge_prep_kernel");
 }
 
 template <int KERNEL>
@@ -256,15 +438,20 @@ extern "C" int hhsar_merge_level(const hhsar_grid_desc *parent_grids, int64_t n_
     cudaStream_t s = as_stream(stream);
     auto kv = reinterpret_cast<const float2 *>(values_in);
     auto out = reinterpret_cast<float2 *>(values_out);
+    MergeChild *kids = nullptr;
+    int rc = prep_children(child_grids, n_child_grids, *geom, kernel, &kids, s);
+    if (rc != HHSAR_OK) return rc;
     if (kernel == 0)
         merge_level_kernel<0><<<blocks, MERGE_THREADS, 0, s>>>(
-            parent_grids, (int)n_parents, n_parent_points, positions, valid, child_grids, fanout,
+            parent_grids, (int)n_parents, n_parent_points, positions, valid, kids, fanout,
             kv, *geom, downconvert, out, flagged);
     else
         merge_level_kernel<1><<<blocks, MERGE_THREADS, 0, s>>>(
-            parent_grids, (int)n_parents, n_parent_points, positions, valid, child_grids, fanout,
+            parent_grids, (int)n_parents, n_parent_points, positions, valid, kids, fanout,
             kv, *geom, downconvert, out, flagged);
-    return check_launch("merge_level_kernel");
+    rc = check_launch("merge_level_kernel");
+    cudaFreeAsync(kids, s);
+    return rc;
 }
 
 extern "C" int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_points,
@@ -292,15 +479,20 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
     cudaStream_t s = as_stream(stream);
     auto kv = reinterpret_cast<const float2 *>(child_values);
     auto o = reinterpret_cast<float2 *>(out);
+    MergeChild *kids = nullptr;
+    int rc = prep_children(child_grids, n_children, *geom, kernel, &kids, s);
+    if (rc != HHSAR_OK) return rc;
     if (kernel == 0)
         merge_cartesian_kernel<0><<<blocks, MERGE_THREADS, 0, s>>>(
             origin[0], origin[1], origin[2], step[0], step[1], step[2], (int)dims[0], (int)dims[1],
-            (int)dims[2], vox_begin, vox_end, child_grids, (int)n_children, kv, *geom, o, flagged);
+            (int)dims[2], vox_begin, vox_end, kids, (int)n_children, kv, *geom, o, flagged);
     else
         merge_cartesian_kernel<1><<<blocks, MERGE_THREADS, 0, s>>>(
             origin[0], origin[1], origin[2], step[0], step[1], step[2], (int)dims[0], (int)dims[1],
-            (int)dims[2], vox_begin, vox_end, child_grids, (int)n_children, kv, *geom, o, flagged);
-    return check_launch("merge_cartesian_kernel");
+            (int)dims[2], vox_begin, vox_end, kids, (int)n_children, kv, *geom, o, flagged);
+    rc = check_launch("merge_cartesian_kernel");
+    cudaFreeAsync(kids, s);
+    return rc;
 }
 
 extern "C" int hhsar_lattice_interp(const void *values, int64_t nu, int64_t nv, int64_t nn,
