@@ -1,11 +1,14 @@
 // Level-1 subimages, point-list form (reference: ffbp.py:310-348).
 //
 // 1. compact_leaf_kernel: per leaf grid, an ordered list of its valid
-//    lattice points (block scan; lattice order keeps a CTA's points compact:
-//    a few (u, v) columns, n fastest).
+//    lattice points (block scan) in n-major order, so a CTA's points lie in a
+//    thin range shell around the leaf's subaperture.
 // 2. leaf_points_kernel: CTA = (leaf, chunk of 256 x P compacted points).
 //    Same unit as the Cartesian BPA tile kernel: per element a delay window
-//    of TW bins covering the chunk's bounding box is staged in shared memory
+//    of TW bins is staged in shared memory, bounded by the triangle
+//    inequality |p - e| in [|p - c| - |e - c|, |p - c| + |e - c|] around the
+//    leaf centre c over the chunk's points (TW = 32 ... 256 chosen per CTA
+//    from the shell thickness and the leaf's element box); the window is
 //    pre-rotated by the carrier, points are processed in pairs with packed
 //    fp32x2 arithmetic; elements whose window does not fit take a checked
 //    global-gather path (reference skip-and-count semantics).  Epilogue:
@@ -30,12 +33,17 @@ compact_leaf_kernel(const hhsar_grid_desc *__restrict__ grids, const uint8_t *__
                     int32_t *__restrict__ idx, int32_t *__restrict__ cnt) {
     __shared__ int s_warp[LP_THREADS / 32];
     const hhsar_grid_desc &D = grids[blockIdx.x];
-    const int npts = D.dims[0] * D.dims[1] * D.dims[2];
+    const int nuv = D.dims[0] * D.dims[1], nn = D.dims[2];
+    const int npts = nuv * nn;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int running = 0;
     for (int c0 = 0; c0 < npts; c0 += LP_THREADS) {
-        const int i = c0 + threadIdx.x;
-        const bool f = i < npts && valid[D.offset + i];
+        // enumerate n-major: a chunk of the list is one or two n layers, i.e.
+        // a thin shell of range around the leaf (tight delay windows)
+        const int j = c0 + threadIdx.x;
+        const int layer = j / nuv;
+        const int i = (j - layer * nuv) * nn + layer;
+        const bool f = j < npts && valid[D.offset + i];
         const unsigned ball = __ballot_sync(0xffffffffu, f);
         if (lane == 0) s_warp[wid] = __popc(ball);
         __syncthreads();
@@ -51,25 +59,35 @@ compact_leaf_kernel(const hhsar_grid_desc *__restrict__ grids, const uint8_t *__
     if (threadIdx.x == 0) cnt[blockIdx.x] = running;
 }
 
+__device__ unsigned long long g_leaf_checked;  // (CTA, element) pairs on the checked path
+
+// Carrier rotation per delay bin, exp(j k_ref c (t0 + dt bin)), float64 phase
+// reduced then rounded once: shared by every element's window staging.
+__global__ void leaf_rot_kernel(float2 *__restrict__ rot, int n_t, double kc_t0, double alpha_d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_t) rot[i] = cis_reduced(kc_t0 + alpha_d * (double)i);
+}
+
 __device__ __forceinline__ float lp_sqrt(float x) {
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
-template <int P, int TW>
+template <int P>
 __global__ void __launch_bounds__(LP_THREADS)
 leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
                    const int32_t *__restrict__ idx, const int32_t *__restrict__ cnt,
                    const double *__restrict__ positions, const float4 *__restrict__ el,
-                   const float2 *__restrict__ env, LeafFast k, hhsar_geom g, int downconvert,
-                   float2 *__restrict__ values, int64_t *__restrict__ oow_total) {
+                   const float2 *__restrict__ env, const float2 *__restrict__ rot, LeafFast k,
+                   hhsar_geom g, int downconvert, float2 *__restrict__ values,
+                   int64_t *__restrict__ oow_total) {
     static_assert(P % 2 == 0, "points are processed in pairs");
-    constexpr int LP_CHUNK = 2048 / TW;  // elements per staging pass: 32 KB of windows
-    __shared__ float4 s_env[LP_CHUNK * TW];
-    __shared__ float4 s_el[LP_CHUNK];
-    __shared__ int s_lo[LP_CHUNK];
-    __shared__ float s_box[6][LP_THREADS / 32];
+    constexpr int WIN = 2048;  // staged window bins per pass: 32 KB
+    __shared__ float4 s_env[WIN];
+    __shared__ float4 s_el[WIN / 32];
+    __shared__ int s_lo[WIN / 32];
+    __shared__ float s_box[2][LP_THREADS / 32];
     const int gi = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
     const hhsar_grid_desc &D = grids[gi];
     const int n = cnt[gi];
@@ -79,7 +97,10 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     // my points (strided so a warp's loads are contiguous)
     float px[P], py[P], pz[P];
     int lat[P];
-    float mn[3] = {3e38f, 3e38f, 3e38f}, mx[3] = {-3e38f, -3e38f, -3e38f};
+    // leaf centre (element bbox midpoint) and the chunk's range shell around it
+    const float cx = (float)(0.5 * (D.box[0] + D.box[3])), cy = (float)(0.5 * (D.box[1] + D.box[4]));
+    const float cz = (float)(0.5 * (D.box[2] + D.box[5]));
+    float dmin = 3e38f, dmax = 0.f;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
         const int li = p0 + q * LP_THREADS + t;
@@ -89,36 +110,45 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         px[q] = (float)pp[0];
         py[q] = (float)pp[1];
         pz[q] = (float)pp[2];
-        mn[0] = fminf(mn[0], px[q]);
-        mx[0] = fmaxf(mx[0], px[q]);
-        mn[1] = fminf(mn[1], py[q]);
-        mx[1] = fmaxf(mx[1], py[q]);
-        mn[2] = fminf(mn[2], pz[q]);
-        mx[2] = fmaxf(mx[2], pz[q]);
+        const float ex = px[q] - cx, ey = py[q] - cy, ez = pz[q] - cz;
+        const float dc = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+        dmin = fminf(dmin, dc);
+        dmax = fmaxf(dmax, dc);
     }
-    // block bounding box of the chunk's points
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        for (int o = 16; o > 0; o >>= 1) {
-            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
-            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
-        }
-        if ((t & 31) == 0) {
-            s_box[a][t >> 5] = mn[a];
-            s_box[3 + a][t >> 5] = mx[a];
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+        dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((t & 31) == 0) {
+        s_box[0][t >> 5] = dmin;
+        s_box[1][t >> 5] = dmax;
     }
     __syncthreads();
-    float b0[3], b1[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        b0[a] = s_box[a][0];
-        b1[a] = s_box[3 + a][0];
-        for (int w = 1; w < LP_THREADS / 32; ++w) {
-            b0[a] = fminf(b0[a], s_box[a][w]);
-            b1[a] = fmaxf(b1[a], s_box[3 + a][w]);
-        }
+    dmin = s_box[0][0];
+    dmax = s_box[1][0];
+    for (int w = 1; w < LP_THREADS / 32; ++w) {
+        dmin = fminf(dmin, s_box[0][w]);
+        dmax = fmaxf(dmax, s_box[1][w]);
     }
+    // window width for this chunk (block-uniform): the widest window any of
+    // the leaf's elements needs (same bounds as the staging below)
+    int need = 0;
+    for (int64_t j = t; j < D.stop - D.start; j += LP_THREADS) {
+        const float4 e = el[D.start + j];
+        const float ex = e.x - cx, ey = e.y - cy, ez = e.z - cz;
+        const float re = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+        const float xlo = fmaxf(dmin - re, 0.f) * k.inv_bin - k.x0;
+        const float xhi = (dmax + re) * k.inv_bin - k.x0;
+        if (xlo >= 1.f && xhi <= k.xmax - 1.f)
+            need = max(need, min((int)floorf(xhi) + 2, k.n_t - 1) - max((int)floorf(xlo) - 2, 0) + 1);
+    }
+    need = __reduce_max_sync(0xffffffffu, need);
+    __syncthreads();  // s_box reads above are done
+    if ((t & 31) == 0) s_box[0][t >> 5] = __int_as_float(need);
+    __syncthreads();
+    for (int w = 0; w < LP_THREADS / 32; ++w) need = max(need, __float_as_int(s_box[0][w]));
+    const int lw = need <= 32 ? 5 : need <= 64 ? 6 : need <= 128 ? 7 : 8;  // log2 TW
+    const int TW = 1 << lw, LP_CHUNK = WIN >> lw;
     f2x pa[P], pb[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) pa[q] = pb[q] = pk2(0.f, 0.f);
@@ -129,14 +159,10 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         __syncthreads();
         if (t < cn) {
             const float4 e = el[e0 + c0 + t];
-            const float qx = fminf(fmaxf(e.x, b0[0]), b1[0]) - e.x;
-            const float qy = fminf(fmaxf(e.y, b0[1]), b1[1]) - e.y;
-            const float qz = fminf(fmaxf(e.z, b0[2]), b1[2]) - e.z;
-            const float fx = fmaxf(fabsf(e.x - b0[0]), fabsf(e.x - b1[0]));
-            const float fy = fmaxf(fabsf(e.y - b0[1]), fabsf(e.y - b1[1]));
-            const float fz = fmaxf(fabsf(e.z - b0[2]), fabsf(e.z - b1[2]));
-            const float xlo = sqrtf(qx * qx + qy * qy + qz * qz) * k.inv_bin - k.x0;
-            const float xhi = sqrtf(fx * fx + fy * fy + fz * fz) * k.inv_bin - k.x0;
+            const float ex = e.x - cx, ey = e.y - cy, ez = e.z - cz;
+            const float re = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+            const float xlo = fmaxf(dmin - re, 0.f) * k.inv_bin - k.x0;
+            const float xhi = (dmax + re) * k.inv_bin - k.x0;
             const int lo = max((int)floorf(xlo) - 2, 0);
             const int hi = min((int)floorf(xhi) + 2, k.n_t - 1);
             const bool fast = xlo >= 1.f && xhi <= k.xmax - 1.f && hi - lo + 1 <= TW;
@@ -146,13 +172,13 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         }
         __syncthreads();
         for (int q = t; q < cn * TW; q += LP_THREADS) {
-            const int j = q / TW, lo = s_lo[j];
+            const int j = q >> lw, lo = s_lo[j];
             if (lo < 0) continue;
-            const int bin = lo + (q % TW);
+            const int bin = lo + (q & (TW - 1));
             const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
             const float2 v0 = __ldg(row + min(bin, k.n_t - 1));
             const float2 v1 = __ldg(row + min(bin + 1, k.n_t - 1));
-            const float2 r = cis_reduced(k.kc_t0 + k.alpha_d * (double)bin);
+            const float2 r = __ldg(rot + bin);
             const float2 dv = bin < k.n_t - 1 ? make_float2(v1.x - v0.x, v1.y - v0.y)
                                               : make_float2(0.f, 0.f);
             const float2 a = cmul(v0, r), b2 = cmul(dv, r);
@@ -192,6 +218,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
                     pb[q + 1] = fma2(v1, bc2(s1), pb[q + 1]);
                 }
             } else {
+                if (t == 0) atomicAdd(&g_leaf_checked, 1ull);
                 // checked path: exact reference skip-and-count, global gathers
                 const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
 #pragma unroll
@@ -248,32 +275,33 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
     k.rev = (float)(k_ref / 3.141592653589793);
     k.n_t = (int)n_t;
     int32_t *idx = nullptr, *cnt = nullptr;
+    float2 *rot = nullptr;
     const int64_t pool = pool_end;  // idx is indexed by global lattice offsets
     if (cudaMallocAsync(&idx, pool * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(&cnt, n_grids * sizeof(int32_t), s) != cudaSuccess)
+        cudaMallocAsync(&cnt, n_grids * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(&rot, n_t * sizeof(float2), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "leaf_bp: scratch allocation failed");
+    leaf_rot_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(rot, (int)n_t, k.kc_t0, k.alpha_d);
     // masked lattice points carry 0 (ffbp.py:174-175); valid ones are written below
     cudaMemsetAsync(values + pool_begin, 0, (pool_end - pool_begin) * sizeof(float2), s);
     compact_leaf_kernel<<<(unsigned)n_grids, LP_THREADS, 0, s>>>(grids, valid, idx, cnt);
     const int chunks = (int)((max_points + LP_THREADS * P - 1) / (LP_THREADS * P));
-    // window width: a chunk's points span up to the region's depth + lateral
-    // extent; in delay bins that is ~ (region diagonal) / (c dt / 2)
-    const double rd = sqrt(pow(g.region[1] - g.region[0], 2) + pow(g.region[3] - g.region[2], 2) +
-                           pow(g.region[5] - g.region[4], 2));
-    const double bins = 1.25 * rd * 2.0 / (HHSAR_C_LIGHT * dt) + 6.0;  // + pad-shell overhang
     const unsigned blocks = (unsigned)(n_grids * chunks);
-    if (bins <= 64)
-        leaf_points_kernel<P, 64><<<blocks, LP_THREADS, 0, s>>>(
-            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
-    else if (bins <= 128)
-        leaf_points_kernel<P, 128><<<blocks, LP_THREADS, 0, s>>>(
-            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
-    else
-        leaf_points_kernel<P, 256><<<blocks, LP_THREADS, 0, s>>>(
-            grids, chunks, idx, cnt, positions, el, env, k, g, downconvert, values, oow_total);
+    leaf_points_kernel<P><<<blocks, LP_THREADS, 0, s>>>(
+        grids, chunks, idx, cnt, positions, el, env, rot, k, g, downconvert, values, oow_total);
     cudaFreeAsync(idx, s);
     cudaFreeAsync(cnt, s);
+    cudaFreeAsync(rot, s);
     return check_launch("leaf_points_kernel");
 }
 
 }  // namespace hhsar
+
+// Diagnostics (not part of the product ABI): number of (CTA, element) pairs
+// that took the checked global-gather path since the last call.
+extern "C" unsigned long long hhsar_debug_leaf_checked(void) {
+    unsigned long long v = 0, z = 0;
+    cudaMemcpyFromSymbol(&v, hhsar::g_leaf_checked, sizeof(v));
+    cudaMemcpyToSymbol(hhsar::g_leaf_checked, &z, sizeof(z));
+    return v;
+}

@@ -81,6 +81,13 @@ def main():
            "leaf_units": int(sum(stats[g, 2] * (run.lattices.descs['stop'][g] - run.lattices.descs['start'][g])
                                 for g in range(*run.sched.level_slices[0]))),
            "flags": flags.tolist(), "sim_s": round(t_sim, 2), "runs": res[1:]}
+    a, b = run.sched.level_slices[0]
+    lp = stats[a:b, 2].astype(np.int64)
+    le = (run.lattices.descs["stop"][a:b] - run.lattices.descs["start"][a:b]).astype(np.int64)
+    slots = int((np.ceil(lp / 1024.0) * 1024).sum())
+    out["leaf_grids"] = {"count": int(b - a), "points_min": int(lp.min()), "points_mean": float(lp.mean()),
+                         "points_max": int(lp.max()), "elements_mean": float(le.mean()),
+                         "slot_fill_at_1024": round(float(lp.sum()) / max(slots, 1), 3)}
     best = min(r["total_ms"] for r in res[1:])
     out["best_ms"] = best
     out["bpa_equiv_gunits_per_s"] = round(w.n_voxels * w.n_elements / (best / 1e3) / 1e9, 1)
