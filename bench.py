@@ -265,9 +265,10 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (262 MB profiles per step)"},
             "volumes_per_s": round(1e3 / ms, 3),
             "e2e": e2e, "roofline": roofline, "clocks": csum,
-            "gpu_launches": 2 * args.steps,
-            "gpu_launches_note": "per step: hhsar_range_demod + hhsar_bpa_cartesian (cuFFT "
-                                 "kernels not counted)",
+            "gpu_launches": 4 * args.steps,
+            "gpu_launches_note": "per step: rc_tables_kernel + range_compress_kernel "
+                                 "(hhsar_range_compress) + bpa_tile_kernel + add_parts_kernel "
+                                 "(hhsar_bpa_cartesian)",
         }
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"], result["parity"] = cpu_baseline_leg(w, out[:ve - vb], dt, k_ref)
