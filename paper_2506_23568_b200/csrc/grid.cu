@@ -360,17 +360,18 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                              z <= D.slack_hi[2];
             bool post = pre;
             if (pre && D.is_leaf) {
-                // 2 * max corner distance / c <= window_hi (ffbp.py:320-330)
-                double dmax = 0.0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const double cx = (b & 4) ? D.box[3] : D.box[0];
-                    const double cy = (b & 2) ? D.box[4] : D.box[1];
-                    const double cz = (b & 1) ? D.box[5] : D.box[2];
-                    const double d =
-                        xsqrt(xadd(xadd(xsq(xsub(x, cx)), xsq(xsub(y, cy))), xsq(xsub(z, cz))));
-                    dmax = fmax(dmax, d);
-                }
+                // 2 * max corner distance / c <= window_hi (ffbp.py:320-330).
+                // The farthest of the 8 corners takes, per axis, the bound
+                // farther from the point; rounded subtraction, squaring,
+                // addition and sqrt are all monotone, so its rounded distance
+                // IS the reference's max over the 8 (bit-exact, 1 sqrt not 8).
+                const double ex0 = xsub(x, D.box[0]), ex1 = xsub(x, D.box[3]);
+                const double ey0 = xsub(y, D.box[1]), ey1 = xsub(y, D.box[4]);
+                const double ez0 = xsub(z, D.box[2]), ez1 = xsub(z, D.box[5]);
+                const double fx = fabs(ex0) >= fabs(ex1) ? ex0 : ex1;
+                const double fy = fabs(ey0) >= fabs(ey1) ? ey0 : ey1;
+                const double fz = fabs(ez0) >= fabs(ez1) ? ez0 : ez1;
+                const double dmax = xsqrt(xadd(xadd(xsq(fx), xsq(fy)), xsq(fz)));
                 post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
             }
             const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
