@@ -180,9 +180,9 @@ int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_
  * (leaf grids) delay-window masks.  positions float64 [P][3], valid uint8
  * [P] (P = sum of lattice sizes, at desc.offset; the caller zeroes valid,
  * inactive columns are never touched), stats int64
- * [n_grids][HHSAR_GRID_STATS] (zeroed by the caller).  block_grid int32
- * [ceil(n_cols / 128)]: the grid of each 128-column block's first column
- * (host-built from col_offset; device pointer). */
+ * [n_grids][HHSAR_GRID_STATS] (zeroed by the caller).  block_grid: optional
+ * int32 [ceil(n_cols / 128)], the grid of each 128-column block's first
+ * column (device pointer); NULL = the kernel binary-searches col_offset. */
 int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_cols,
                       const int32_t *block_grid, const hhsar_geom *geom, double *positions,
                       uint8_t *valid, int64_t *stats, void *stream);

@@ -320,8 +320,18 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         if (!have) {
             const unsigned long long c = atomicAdd(counter, 1ull);
             if (c >= (unsigned long long)n_cols) break;
-            int g2 = block_grid[c >> 7];
-            while (g2 + 1 < n_grids && (unsigned long long)grids[g2 + 1].col_offset <= c) ++g2;
+            int g2;
+            if (block_grid) {
+                g2 = block_grid[c >> 7];
+                while (g2 + 1 < n_grids && (unsigned long long)grids[g2 + 1].col_offset <= c) ++g2;
+            } else {  // last grid whose col_offset <= c (empty grids share the next offset)
+                int lo = 0, hi = n_grids - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if ((unsigned long long)grids[mid].col_offset <= c) lo = mid; else hi = mid - 1;
+                }
+                g2 = lo;
+            }
             if (g2 != acc_gi) {
                 flush();
                 acc_gi = g2;
@@ -450,7 +460,6 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
                                  double *positions, uint8_t *valid, int64_t *stats,
                                  void *stream) {
     HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
-    HHSAR_REQUIRE(n_cols == 0 || block_grid != nullptr, "grid_newton: block_grid required");
     if (n_cols == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
     static int per_sm = 0;

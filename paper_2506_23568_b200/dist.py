@@ -179,7 +179,7 @@ def plan_shard(n_elements: int, levels: int, merge_factor: int, world: int, rank
     owned element rows [e0, e1)).  kx = -1 when no level splits evenly (then
     every rank builds every subtree and only the landing is sharded)."""
     from .ffbp import Schedule
-    sched = Schedule(n_elements, levels, merge_factor)
+    sched = Schedule.shared(int(n_elements), levels, merge_factor)
     n_lv = len(sched.level_slices)
     kx = exchange_level(sched, world) if world > 1 else n_lv - 1
     if kx is None:

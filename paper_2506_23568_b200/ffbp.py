@@ -28,6 +28,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import functools
+
 import numpy as np
 
 from . import _native
@@ -87,6 +89,15 @@ class Schedule:
     Subarray j of 1-based tree level L covers leaves [j 2^(L-1), (j+1) 2^(L-1))
     (model.py:383-386 pairs consecutive children).
     """
+
+    @staticmethod
+    @functools.lru_cache(maxsize=16)
+    def shared(n_elements: int, levels: int, merge_factor: int = 2) -> "Schedule":
+        """Memoised, read-only schedule (a pure function of three integers)."""
+        sc = Schedule(n_elements, levels, merge_factor)
+        for a in (sc.grids, sc.bounds):
+            a.setflags(write=False)
+        return sc
 
     def __init__(self, n_elements: int, levels: int, merge_factor: int = 2):
         s = int(round(np.log2(merge_factor)))
@@ -230,42 +241,55 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
                 done=done, keep=(staged, up, leaf_box))
 
 
+_trace = None  # optional host-timeline hook (tools/host_overhead.py)
+
+
 def finish_lattices(p, newton_grids=None) -> Lattices:
     """Wait for the plan, size the pools, launch Newton (current stream)."""
     import torch
     p["done"].synchronize()
+    if _trace:
+        _trace("plan synced")
     sched, descs_dev, geom = p["sched"], p["descs_dev"], p["geom"]
     dev = descs_dev.device
     stream = _native.stream_handle()
-    host = np.frombuffer(p["host_d"].numpy().tobytes(), dtype=_native.GRID_DTYPE).copy()
+    host = p["host_d"].numpy().copy().view(_native.GRID_DTYPE)  # byte copy, then the record view
     if int(p["host_s"][0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
     dims = host["dims"].astype(np.int64)
-    npts = dims.prod(axis=1)
-    host["offset"] = np.concatenate([[0], np.cumsum(npts)[:-1]])
-    # Newton work list: the active (u, v) rectangle of every grid
+    npts = dims[:, 0] * dims[:, 1] * dims[:, 2]
+    offsets = np.cumsum(npts)
+    total = int(offsets[-1])
+    host["offset"][0] = 0
+    host["offset"][1:] = offsets[:-1]
+    # Newton work list: the active (u, v) rectangle of every grid (the kernel
+    # finds a column's grid by binary search over col_offset)
     span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
     cols = span[:, 0] * span[:, 1]
     if newton_grids is not None:
         cols = np.where(np.asarray(newton_grids, dtype=bool), cols, 0)
-    starts = np.concatenate([[0], np.cumsum(cols)[:-1]])
-    host["col_offset"] = starts
-    n_cols = int(cols.sum())
-    block_grid = np.searchsorted(starts, np.arange(0, max(n_cols, 1), 128), side="right") - 1
-    # descriptors + Newton block table go up in one pinned, asynchronous copy
-    blob = np.concatenate([host.view(np.uint8).reshape(-1),
-                           block_grid.astype(np.int32).view(np.uint8)])
-    staged = torch.from_numpy(blob).pin_memory()
-    up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
-    up.copy_(staged, non_blocking=True)
-    descs_dev = up[:host.nbytes]
-    bg = up[host.nbytes:]
-    total = int(npts.sum())
+    starts = np.cumsum(cols)
+    n_cols = int(starts[-1])
+    host["col_offset"][0] = 0
+    host["col_offset"][1:] = starts[:-1]
+    if _trace:
+        _trace("worklist built")
+    # descriptors go back up through the plan's pinned staging buffer (its
+    # upload completed before the plan ran) into the plan's device copy
+    staged, up = p["keep"][0], p["keep"][1]
+    nb = host.nbytes
+    staged.numpy()[:nb] = host.view(np.uint8).reshape(-1)
+    up[:nb].copy_(staged[:nb], non_blocking=True)
+    descs_dev = up[:nb]
+    if _trace:
+        _trace("descs uploaded")
     positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
     valid = torch.zeros(total, dtype=torch.uint8, device=dev)
     stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
+    if _trace:
+        _trace("pools allocated")
     _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, n_cols,
-                 _native.ptr(bg), _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
+                 None, _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
                  _native.ptr(stats), stream)
     lat = Lattices(host, descs_dev, positions, valid, stats, geom)
     lat.keep = (staged, up)  # pinned staging must outlive the async copy
@@ -304,7 +328,7 @@ class Pipeline:
         self.kid = _kernel_id(params.kernel)
         if window_hi is None:
             window_hi = t0 + (env.shape[1] - 1) * dt
-        self.sched = sched or Schedule(el_dev.shape[0], levels, merge_factor)
+        self.sched = sched or Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
         self.lat = lat or build_lattices(el_dev, self.sched, region, kgrid, params.gamma,
                                          params.margin, src_pad_of(params), window_hi,
                                          newton_grids=newton_grids)
@@ -418,7 +442,7 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     # range compression first: it needs no host preparation and hides the
     # schedule / plan set-up below
     env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
-    sched = Schedule(el_dev.shape[0], levels, merge_factor)
+    sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)

@@ -32,6 +32,7 @@ def traced(name, *a):
 
 
 _native.call = traced
+ffbp._trace = lambda label: log.append((label, time.perf_counter(), time.perf_counter()))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t0 = time.perf_counter()
 e0.record()
