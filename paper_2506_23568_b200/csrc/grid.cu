@@ -472,7 +472,16 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     if (cudaMallocAsync(&counter, sizeof(unsigned long long), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "grid_newton: counter allocation failed");
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
-    int64_t blocks = (int64_t)sm_count() * per_sm;
+    // Lanes own whole columns (warm starts chain along n), so the kernel ends
+    // when the last long column does: keep ~COLS columns per lane for the
+    // balance, within [1, occupancy] CTAs per SM.
+    const char *cpl = getenv("HHSAR_NEWTON_CPL");  // experiment knob
+    const int64_t COLS = cpl ? atoi(cpl) : 4;
+    int64_t bps = (n_cols + COLS * NEWTON_THREADS * sm_count() / 2) /
+                  (COLS * NEWTON_THREADS * sm_count());  // whole CTAs per SM (even spread)
+    if (bps > per_sm) bps = per_sm;
+    if (bps < 1) bps = 1;
+    int64_t blocks = bps * sm_count();
     const int64_t need = (n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS;
     if (blocks > need) blocks = need;
     grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
