@@ -18,6 +18,8 @@
  *                             (bpa.py:163-176)
  *   hhsar_range_demod      <- rangecomp.range_compress's pad + demodulation
  *                             (rangecomp.py:86-96; the IDFT itself is cuFFT)
+ *   hhsar_volume_dot / hhsar_volume_residual <- metrics.psnr (metrics.py:126-150)
+ *   hhsar_mip              <- metrics.max_intensity_projection (metrics.py:170-190)
  *   hhsar_leaf_boxes / hhsar_grid_plan / hhsar_grid_newton
  *                          <- ffbp.build_subimage_grid for every subarray of
  *                             every level at once (ffbp.py:179-307) plus the
@@ -243,6 +245,26 @@ int hhsar_merge_cartesian(const double *origin, const double *step, const int64_
 int hhsar_simulate(const double *el_pos, int64_t n_el, const double *pos,
                    const double *refl, int64_t n_s, const double *k, int64_t n_f,
                    void *out, void *stream);
+
+/* ---- image-quality metrics ------------------------------ */
+
+/* psnr (metrics.py:126-150), pass 1: out5 (device, float64) = [sum |t|^2,
+ * Re sum conj(t) r, Im sum conj(t) r, sum |r|^2, max |r|] over n complex
+ * samples (dtype 0 = complex64, 1 = complex128), float64 accumulation in a
+ * fixed reduction order.  np.vdot(tst, ref) = out5[1] + j out5[2]. */
+int hhsar_volume_dot(const void *test, const void *ref, int64_t n, int dtype, double *out5,
+                     void *stream);
+
+/* psnr pass 2: out1 (device) = sum |s t - r|^2 for the complex scale s. */
+int hhsar_volume_residual(const void *test, const void *ref, int64_t n, int dtype,
+                          double scale_re, double scale_im, double *out1, void *stream);
+
+/* max_intensity_projection (metrics.py:170-190): out (device, float64) =
+ * per-pixel max |v| along `axis` of the [dims[0]][dims[1]][dims[2]] volume
+ * (dims host), dB-scaled to its own peak, clipped at floor_db < 0 and mapped
+ * onto [0, 1]; an all-zero volume gives zeros. */
+int hhsar_mip(const void *volume, const int64_t *dims, int dtype, int axis, double floor_db,
+              double *out, void *stream);
 
 #ifdef __cplusplus
 }

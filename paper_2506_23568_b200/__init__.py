@@ -18,6 +18,8 @@ from .ffbp import (GRID_PAD, FfbpParams, Subimage, SubimageGrid, build_subimage_
                    default_levels, hhffbpa_reconstruct, level1_reconstruct, merge_pair)
 from .model import (C_LIGHT, DataCube, FrequencyGrid, ImagingRegion, Subarray,
                     SubarrayTree, SyntheticAperture, partition_subarrays, validate_geometry)
+from .metrics import (PSNR_SENTINEL_DB, PsfReport, max_intensity_projection, profile_cut,
+                      psf_metrics, psnr)
 from .rangecomp import RangeProfileSet, range_compress
 from .spectrum import SubarrayExtents, default_grid_dims
 
@@ -26,9 +28,10 @@ __version__ = "0.1.0"
 __all__ = [
     "C_LIGHT", "ConfigError", "DataCube", "FfbpParams", "FrequencyGrid", "GRID_PAD",
     "HhsarError", "ImageVolume", "ImagingRegion", "IoFormatError", "NativeUnavailableError",
-    "NumericDomainError", "RangeProfileSet", "Subarray", "SubarrayExtents", "SubarrayTree",
+    "NumericDomainError", "PSNR_SENTINEL_DB", "PsfReport", "RangeProfileSet", "Subarray", "SubarrayExtents", "SubarrayTree",
     "Subimage", "SubimageGrid", "SyntheticAperture", "backproject", "backproject_gather",
     "bpa_reconstruct", "build_subimage_grid", "check_delay_window", "default_grid_dims",
-    "default_levels", "hhffbpa_reconstruct", "level1_reconstruct", "merge_pair",
-    "partition_subarrays", "range_compress", "region_grid", "validate_geometry",
+    "default_levels", "hhffbpa_reconstruct", "level1_reconstruct", "max_intensity_projection",
+    "merge_pair", "partition_subarrays", "profile_cut", "psf_metrics", "psnr", "range_compress",
+    "region_grid", "validate_geometry",
 ]

@@ -18,6 +18,8 @@ medium   the `medium` fixture (conftest.py:103-114): 17x17, dims (33,33,17),
 config0  BASELINE config 0 (paper_2506_23568_b200.workloads.config(0)): BPA
          64x64x32, HHFFBPA binary M=7 and the merge-factor-4 schedule built
          from reference primitives; all grid masks.
+metrics  metrics.py on seeded volumes/profiles (`make_golden.py metrics`
+         regenerates only this one).
 """
 
 from __future__ import annotations
@@ -277,8 +279,67 @@ def case_io():
     np.savez_compressed(HERE / "io_reference.npz", **out)
 
 
+def case_metrics():
+    """metrics.py outputs (psnr, max_intensity_projection, psf_metrics,
+    profile_cut) on seeded volumes and profiles; error messages of the
+    rejected inputs."""
+    from hhsar.bpa import ImageVolume
+    from hhsar import metrics as rm
+    rng = np.random.default_rng(2026)
+    dims = (12, 10, 9)
+    origin, step = np.array([-0.05, -0.04, 0.2]), np.array([0.01, 0.009, 0.012])
+    ref = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    ref[5, 4, 3] = 12.0 - 3.0j  # a dominant peak
+    noisy = ref * (0.7 - 0.4j) + 0.05 * (rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+    ref64 = ref.astype(np.complex64)
+    noisy64 = noisy.astype(np.complex64)
+    out = {"dims": np.array(dims), "origin": origin, "step": step, "ref": ref, "noisy": noisy,
+           "ref64": ref64, "noisy64": noisy64}
+    V = lambda v: ImageVolume(v, origin, step)  # noqa: E731
+    out["psnr_noisy"] = rm.psnr(V(ref), V(noisy))
+    out["psnr_noisy64"] = rm.psnr(V(ref64.astype(np.complex128)), V(noisy64.astype(np.complex128)))
+    out["psnr_same"] = rm.psnr(V(ref), V(ref.copy()))
+    out["psnr_scaled"] = rm.psnr(V(ref), V(ref * (0.3 + 2.1j)))
+    out["psnr_zero_test"] = rm.psnr(V(ref), V(np.zeros(dims, complex)))
+    for ax in ("x", "y", "z"):
+        for fl in (-40.0, -25.0):
+            out[f"mip_{ax}_{int(-fl)}"] = rm.max_intensity_projection(V(ref), ax, fl)
+    out["mip_zero"] = rm.max_intensity_projection(V(np.zeros(dims, complex)), 1)
+    # PSF of a sampled sinc-like response (with a sidelobe floor) and a shifted copy
+    x = np.arange(96) - 40.3
+    prof = np.sinc(x / 3.7) * np.exp(0.3j * x) + 1e-3
+    out["psf_profile"] = prof
+    rep = rm.psf_metrics(prof, 0.002)
+    out["psf"] = np.array([rep.mainlobe_width_mm, rep.pslr_db, rep.islr_db, rep.peak_position_m])
+    cut, sp = rm.profile_cut(V(ref), "y", (0.0, 0.0, 0.23))
+    out["cut_y"] = cut
+    out["cut_spacing"] = sp
+    errs = []
+    for fn in (lambda: rm.psf_metrics(np.ones(64, complex), 0.002),
+               lambda: rm.psf_metrics(np.zeros(64, complex), 0.002),
+               lambda: rm.psf_metrics(prof[:3], 0.002),
+               lambda: rm.psf_metrics(prof, 0.0),
+               lambda: rm.psf_metrics(np.exp(-np.linspace(-2, 2, 65) ** 2).astype(complex), 0.01),
+               lambda: rm.psf_metrics(np.array([8.2, 8.0, 8.5, 8.6, 9.0, 8.7, 8.1, 8.3, 1.0], complex), 0.01),
+               lambda: rm.max_intensity_projection(V(ref), "w"),
+               lambda: rm.max_intensity_projection(V(ref), 3),
+               lambda: rm.max_intensity_projection(V(ref), "z", 0.0),
+               lambda: rm.psnr(V(ref), ImageVolume(ref, origin + 1.0, step))):
+        try:
+            fn()
+            errs.append("")
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"{type(e).__name__}: {e}")
+    out["errors"] = np.array(errs)
+    np.savez_compressed(HERE / "metrics.npz", **out)
+
+
 def main():
+    if sys.argv[1:] == ["metrics"]:
+        case_metrics()
+        return
     case_io()
+    case_metrics()
     for name, fn in (("small", case_small), ("medium", case_medium), ("config0", case_config0)):
         out = {}
         fn(out)

@@ -13,6 +13,11 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
 @lru_cache(maxsize=None)
+def load_npz(name: str) -> dict:
+    """The raw arrays of a golden file (cases without an aperture/cube)."""
+    return dict(np.load(GOLDEN / f"{name}.npz"))
+
+
 def load(name: str) -> SimpleNamespace:
     z = dict(np.load(GOLDEN / f"{name}.npz"))
     f = z["freqs"]

@@ -155,3 +155,52 @@ def test_product_path_fails_loudly_without_gpu(monkeypatch):
                           w.freqs)
     with pytest.raises(NativeUnavailableError):
         bpa_reconstruct(cube, w.region, dims=(4, 4, 4))
+
+
+# ---- metrics: host-side parts (psf_metrics, profile_cut, argument checks) ----
+
+def test_psf_metrics_matches_reference():
+    from goldens import load_npz as load
+    from paper_2506_23568_b200 import metrics
+    z = load("metrics")
+    rep = metrics.psf_metrics(z["psf_profile"], 0.002)
+    got = np.array([rep.mainlobe_width_mm, rep.pslr_db, rep.islr_db, rep.peak_position_m])
+    assert np.allclose(got, z["psf"], rtol=1e-12, atol=1e-12)
+    assert set(rep.to_dict()) == {"mainlobe_width_mm", "pslr_db", "islr_db", "peak_position_m"}
+
+
+def test_metrics_errors_match_reference():
+    """Same exception classes and messages as the reference for every
+    rejected input (the GPU is never reached: all checks come first)."""
+    from goldens import load_npz as load
+    from paper_2506_23568_b200 import metrics
+    from paper_2506_23568_b200.bpa import ImageVolume
+    z = load("metrics")
+    prof = z["psf_profile"]
+    ref = ImageVolume(z["ref"], z["origin"], z["step"])
+    calls = [lambda: metrics.psf_metrics(np.ones(64, complex), 0.002),
+             lambda: metrics.psf_metrics(np.zeros(64, complex), 0.002),
+             lambda: metrics.psf_metrics(prof[:3], 0.002),
+             lambda: metrics.psf_metrics(prof, 0.0),
+             lambda: metrics.psf_metrics(np.exp(-np.linspace(-2, 2, 65) ** 2).astype(complex),
+                                         0.01),
+             lambda: metrics.psf_metrics(np.array([8.2, 8.0, 8.5, 8.6, 9.0, 8.7, 8.1, 8.3, 1.0],
+                                                  complex), 0.01),
+             lambda: metrics.max_intensity_projection(ref, "w"),
+             lambda: metrics.max_intensity_projection(ref, 3),
+             lambda: metrics.max_intensity_projection(ref, "z", 0.0),
+             lambda: metrics.psnr(ref, ImageVolume(z["ref"], z["origin"] + 1.0, z["step"]))]
+    for fn, want in zip(calls, z["errors"]):
+        with pytest.raises(Exception) as exc:
+            fn()
+        assert f"{type(exc.value).__name__}: {exc.value}" == str(want)
+
+
+def test_profile_cut_matches_reference():
+    from goldens import load_npz as load
+    from paper_2506_23568_b200 import metrics
+    from paper_2506_23568_b200.bpa import ImageVolume
+    z = load("metrics")
+    cut, sp = metrics.profile_cut(ImageVolume(z["ref"], z["origin"], z["step"]), "y",
+                                  (0.0, 0.0, 0.23))
+    assert np.array_equal(cut, z["cut_y"]) and sp == float(z["cut_spacing"])
