@@ -284,6 +284,34 @@ def run_ours(args):
     return result
 
 
+def metrics_leg(volume, dims):
+    """GPU psnr + max-intensity projection of a device volume (SURVEY
+    §8(f) #4): psnr streams both volumes twice (4 x 8 B per voxel), the MIP
+    once; reported against the HBM roofline."""
+    import torch
+    from paper_2506_23568_b200 import metrics
+    test = volume * (0.5 + 0.25j)
+    n = volume.numel()
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t) / reps * 1e3
+
+    ps = timed(lambda: metrics.psnr_device(volume, test))
+    mp = timed(lambda: metrics.mip_device(volume.view(*dims), "z"))
+    value = metrics.psnr_device(volume, test)
+    hbm = measured_peaks().get("hbm_gbs", 6542.1)
+    return {"voxels": int(n), "psnr_db": round(value, 3), "psnr_ms": round(ps, 3),
+            "psnr_gbs": round(4 * 8 * n / ps / 1e6, 1), "mip_ms": round(mp, 3),
+            "mip_gbs": round(8 * n / mp / 1e6, 1), "hbm_peak_gbs": hbm,
+            "note": "host wall time per call incl. two scalar read-backs (psnr)"}
+
+
 def hhffbpa_leg(index, dev, steps, check=False):
     """HHFFBPA on BASELINE config `index` (binary schedule, the reference's
     own): device-resident cube, one step = range compression + grids +
@@ -357,6 +385,8 @@ def hhffbpa_leg(index, dev, steps, check=False):
             "level_points_equal": lp == prov["level_points"][:-1]}
         out["cpu_oracle_s"] = round(t, 2)
         out["cpu_oracle_cores"] = oracle.threads()
+    if big:
+        out["metrics"] = metrics_leg(run.volume, w.dims)
     del run, cube
     torch.cuda.empty_cache()
     return out

@@ -29,6 +29,15 @@ struct Cplx<double2> {
     __device__ static double im(double2 v) { return v.y; }
 };
 
+// |v|^2 in float64; maxima are taken on squares and the (monotone,
+// correctly rounded) sqrt applied once to the result -- within 1 ulp of
+// numpy's hypot for these magnitudes
+template <typename C>
+__device__ __forceinline__ double cabs2_d(C v) {
+    const double a = Cplx<C>::re(v), b = Cplx<C>::im(v);
+    return fma(a, a, b * b);
+}
+
 template <int N>
 __device__ __forceinline__ void block_sum(double (&v)[N], double *s_part) {
 #pragma unroll
@@ -55,6 +64,7 @@ volume_dot_kernel(const C *__restrict__ t, const C *__restrict__ r, int64_t n,
     __shared__ double s_part[4 * MET_THREADS / 32];
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     double mx = 0.0;
+#pragma unroll 4
     for (int64_t i = (int64_t)blockIdx.x * MET_THREADS + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * MET_THREADS) {
         const C a = t[i], b = r[i];
@@ -64,7 +74,7 @@ volume_dot_kernel(const C *__restrict__ t, const C *__restrict__ r, int64_t n,
         v[1] += ar * br + ai * bi;
         v[2] += ar * bi - ai * br;
         v[3] += br * br + bi * bi;
-        mx = fmax(mx, hypot(br, bi));
+        mx = fmax(mx, fma(br, br, bi * bi));
     }
     block_sum(v, s_part);
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -78,7 +88,7 @@ volume_dot_kernel(const C *__restrict__ t, const C *__restrict__ r, int64_t n,
         p[1] = v[1];
         p[2] = v[2];
         p[3] = v[3];
-        p[4] = mx;
+        p[4] = sqrt(mx);
     }
 }
 
@@ -89,6 +99,7 @@ volume_residual_kernel(const C *__restrict__ t, const C *__restrict__ r, int64_t
                        double si, double *__restrict__ partial) {
     __shared__ double s_part[MET_THREADS / 32];
     double v[1] = {0.0};
+#pragma unroll 4
     for (int64_t i = (int64_t)blockIdx.x * MET_THREADS + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * MET_THREADS) {
         const C a = t[i], b = r[i];
@@ -101,19 +112,24 @@ volume_residual_kernel(const C *__restrict__ t, const C *__restrict__ r, int64_t
     if (threadIdx.x == 0) partial[blockIdx.x] = v[0];
 }
 
-// out[k] = sum over CTAs of partial[b * width + k] in CTA order (max for k in
-// max_mask)
+// out[k] = reduction over CTAs of partial[b * width + k] (max for k in
+// max_mask): one warp per column, lanes take CTAs lane, lane + 32, ... and a
+// fixed shuffle tree combines them (deterministic).
 __global__ void reduce_partials_kernel(const double *__restrict__ partial, int nb, int width,
                                        unsigned max_mask, double *__restrict__ out) {
-    const int k = threadIdx.x;
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (k >= width) return;
     const bool is_max = (max_mask >> k) & 1u;
     double a = 0.0;  // sums start at 0; maxima of magnitudes too
-    for (int b = 0; b < nb; ++b) {
+    for (int b = lane; b < nb; b += 32) {
         const double x = partial[(int64_t)b * width + k];
         a = is_max ? fmax(a, x) : a + x;
     }
-    out[k] = a;
+    for (int o = 16; o > 0; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, a, o);
+        a = is_max ? fmax(a, y) : a + y;
+    }
+    if (lane == 0) out[k] = a;
 }
 
 // MIP: out[(a, b)] = max over the projected axis of |v|; dims (n0, n1, n2),
@@ -128,9 +144,10 @@ __global__ void mip_rows_kernel(const C *__restrict__ v, int64_t rows, int64_t n
     if (o >= rows) return;  // warp-uniform
     const C *p = v + o * n2;
     double m = 0.0;
-    for (int64_t k = lane; k < n2; k += 32) m = fmax(m, hypot(Cplx<C>::re(p[k]), Cplx<C>::im(p[k])));
+#pragma unroll 8
+    for (int64_t k = lane; k < n2; k += 32) m = fmax(m, cabs2_d(p[k]));
     for (int s = 16; s > 0; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
-    if (lane == 0) out[o] = m;
+    if (lane == 0) out[o] = sqrt(m);
 }
 
 template <typename C>
@@ -143,26 +160,33 @@ __global__ void mip_strided_kernel(const C *__restrict__ v, int64_t n0, int64_t 
     if (axis == 1) {  // out (i, k) = max_j v[i, j, k]
         const int64_t i = o / n2, k = o % n2;
         const C *p = v + i * n1 * n2 + k;
+#pragma unroll 8
         for (int64_t j = 0; j < n1; ++j)
-            m = fmax(m, hypot(Cplx<C>::re(p[j * n2]), Cplx<C>::im(p[j * n2])));
+            m = fmax(m, cabs2_d(p[j * n2]));
     } else {  // out (j, k) = max_i v[i, j, k]
         const C *p = v + o;
+#pragma unroll 8
         for (int64_t i = 0; i < n0; ++i)
-            m = fmax(m, hypot(Cplx<C>::re(p[i * n1 * n2]), Cplx<C>::im(p[i * n1 * n2])));
+            m = fmax(m, cabs2_d(p[i * n1 * n2]));
     }
-    out[o] = m;
+    out[o] = sqrt(m);
 }
 
-__global__ void max_kernel(const double *__restrict__ x, int64_t n, double *__restrict__ out) {
+// Grid-wide max of non-negative doubles: their bit patterns order like
+// unsigned integers, so one atomicMax per CTA (order-independent, exact).
+__global__ void max_kernel(const double *__restrict__ x, int64_t n,
+                           unsigned long long *__restrict__ out_bits) {
     __shared__ double s[MET_THREADS / 32];
     double m = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += MET_THREADS) m = fmax(m, x[i]);
+    for (int64_t i = (int64_t)blockIdx.x * MET_THREADS + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * MET_THREADS)
+        m = fmax(m, x[i]);
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < MET_THREADS / 32; ++w) m = fmax(m, s[w]);
-        out[0] = m;
+        atomicMax(out_bits, (unsigned long long)__double_as_longlong(m));
     }
 }
 
@@ -183,7 +207,7 @@ __global__ void mip_map_kernel(double *__restrict__ x, int64_t n, const double *
 
 static int metric_blocks(int64_t n) {
     int64_t nb = (n + MET_THREADS - 1) / MET_THREADS;
-    const int64_t cap = 4 * (int64_t)sm_count();
+    const int64_t cap = 8 * (int64_t)sm_count();
     return (int)(nb < cap ? (nb < 1 ? 1 : nb) : cap);
 }
 
@@ -206,7 +230,7 @@ extern "C" int hhsar_volume_dot(const void *test, const void *ref, int64_t n, in
         volume_dot_kernel<double2><<<nb, MET_THREADS, 0, s>>>(
             reinterpret_cast<const double2 *>(test), reinterpret_cast<const double2 *>(ref), n,
             part);
-    reduce_partials_kernel<<<1, 32, 0, s>>>(part, nb, 5, 1u << 4, out5);
+    reduce_partials_kernel<<<1, 5 * 32, 0, s>>>(part, nb, 5, 1u << 4, out5);
     cudaFreeAsync(part, s);
     return check_launch("volume_dot_kernel");
 }
@@ -262,7 +286,9 @@ extern "C" int hhsar_mip(const void *volume, const int64_t *dims, int dtype, int
     double *peak = nullptr;
     if (cudaMallocAsync(&peak, sizeof(double), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "mip: scratch allocation failed");
-    max_kernel<<<1, MET_THREADS, 0, s>>>(out, no, peak);
+    cudaMemsetAsync(peak, 0, sizeof(double), s);  // +0.0
+    max_kernel<<<metric_blocks(no), MET_THREADS, 0, s>>>(
+        out, no, reinterpret_cast<unsigned long long *>(peak));
     mip_map_kernel<<<blocks, MET_THREADS, 0, s>>>(out, no, peak, floor_db);
     cudaFreeAsync(peak, s);
     return check_launch("mip_rows_kernel / mip_strided_kernel");
