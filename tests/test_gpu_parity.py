@@ -295,3 +295,30 @@ def test_gpu_matches_oracle_on_config2_subset(hh):
     assert_image_parity(g.values, o)
     assert g.provenance["level_points"] == prov["level_points"]
     assert g.provenance["merge_flags"] == prov["merge_flags"]
+
+
+def test_config3_full_scale_vs_oracle(hh):
+    """BASELINE config 3 at full scale (131,072 elements, 512x512x128, binary
+    M=11): the device pipeline against the oracle on the same GPU-simulated
+    cube -- image parity, per-grid valid-point counts of every level and the
+    merge flags (~30 s of CPU oracle)."""
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, ffbp, workloads
+    from paper_2506_23568_b200.model import DataCube
+    w = workloads.config(3)
+    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                            w.freqs.k_samples)
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    run = ffbp.hhffbpa_from_cube(cube, el, bpa.el_f32x4(el), w.freqs, w.region, w.dims,
+                                 ffbp.FfbpParams(levels=w.levels), w.levels, 2, w.upsample)
+    torch.cuda.synchronize()
+    host = DataCube(values=cube.cpu().numpy(), aperture=w.aperture, freqs=w.freqs)
+    want, _, _, prov = oracle.hhffbpa_reconstruct(host, w.region, w.dims, levels=w.levels,
+                                                  upsample=w.upsample)
+    got = run.volume.cpu().numpy().reshape(w.dims)
+    assert_image_parity(got, want)
+    stats = run.lattices.stats.cpu().numpy()
+    lp = [[int(v) for v in stats[a:b, 2 if k == 0 else 0]]
+          for k, (a, b) in enumerate(run.sched.level_slices)]
+    assert lp == prov["level_points"][:-1]
+    assert [int(f) for f in run.flags.cpu().numpy()] == prov["merge_flags"] + [prov["final_flags"]]
