@@ -14,12 +14,18 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--frames", type=int, default=None)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--random", action="store_true", help="seeded random cube (no Born sum)")
     args = ap.parse_args()
     import torch
     from paper_2506_23568_b200 import _native, bpa, ffbp, rangecomp, workloads
     w = workloads.config(args.config, frames=args.frames)
-    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
-                            w.freqs.k_samples)
+    if args.random:
+        gen = torch.Generator(device="cuda").manual_seed(w.seed)
+        cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
+                           generator=gen)
+    else:
+        cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                                w.freqs.k_samples)
     el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
     el4 = bpa.el_f32x4(el)
     for _ in range(args.steps):
