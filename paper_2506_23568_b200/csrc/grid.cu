@@ -274,43 +274,201 @@ grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__
 }
 
 // ---- Newton columns -------------------------------------------------------------
-// Persistent kernel with PER-LANE work fetching: every lane runs its own
-// (column, plane, iteration) state machine and, when its column is done,
-// grabs the next one from a global counter.  A column's cost varies >10x
-// (failing planes run 50 iterations), so static one-column-per-thread left
-// ~70% of the lanes idle; here lanes stay busy until the work list drains.
 // Work list = the active columns only (desc.act_* rectangle, see
 // grid_plan_kernel): columns outside the near band are masked whatever
 // Newton returns (ffbp.py:294-301) and unreachable ones provably fail, so
-// neither is launched (the caller zeroed `valid`).
+// neither is launched (the caller zeroed `valid`).  Within a column the
+// reference marches the n planes in order, warm-starting plane w + 1 from
+// plane w's solution when plane w converged and from the region centre
+// otherwise (ffbp.py:274-282).
+//
+// * light columns: persistent kernel with PER-LANE work fetching -- every
+//   lane runs its own (column, plane, iteration) state machine and grabs the
+//   next column from a global counter when done;
+// * heavy columns: segments of planes solved speculatively in parallel, then
+//   a fix-up pass in the reference's order (below).
 constexpr int NEWTON_THREADS = 128;
+constexpr int HEAVY_MAXP = 64;  // planes per heavy column held in shared memory
+
+__device__ __forceinline__ int grid_of_column(const hhsar_grid_desc *__restrict__ grids,
+                                              int n_grids, const int32_t *__restrict__ block_grid,
+                                              unsigned long long c) {
+    if (block_grid) {
+        int g2 = block_grid[c >> 7];
+        while (g2 + 1 < n_grids && (unsigned long long)grids[g2 + 1].col_offset <= c) ++g2;
+        return g2;
+    }
+    int lo = 0, hi = n_grids - 1;  // last grid whose col_offset <= c (empty grids share offsets)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((unsigned long long)grids[mid].col_offset <= c) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+struct Column {
+    int gi, iu, iv;
+    double tu, tv;
+};
+
+__device__ __forceinline__ Column decode_column(const hhsar_grid_desc *__restrict__ grids,
+                                                int n_grids, const int32_t *block_grid,
+                                                const hhsar_geom &g, unsigned long long c) {
+    Column q;
+    q.gi = grid_of_column(grids, n_grids, block_grid, c);
+    const hhsar_grid_desc &D = grids[q.gi];
+    const int k = (int)((int64_t)c - D.col_offset);
+    const int wv = D.act_hi[1] - D.act_lo[1] + 1;
+    const int ku = k / wv;
+    q.iu = D.act_lo[0] + ku;
+    q.iv = D.act_lo[1] + (k - ku * wv);
+    q.tu = xadd(D.origin[0], xmul(g.step, (double)q.iu));
+    q.tv = xadd(D.origin[1], xmul(g.step, (double)q.iv));
+    return q;
+}
+
+__device__ __forceinline__ bool column_is_heavy(const hhsar_grid_desc &D, const hhsar_geom &g,
+                                                double tu, double tv) {
+    const double qu = tu / (g.c_uv * (D.ext[1] - D.ext[0]));
+    const double qv = tv / (g.c_uv * (D.ext[3] - D.ext[2]));
+    return qu * qu + qv * qv >= 1.0 && D.near_hi[2] + 1 <= HEAVY_MAXP;
+}
+
+__device__ __forceinline__ void column_geom(const hhsar_grid_desc &D, const hhsar_geom &g,
+                                            NewtonGeom &G) {
+    G.c_uv = g.c_uv;
+    G.c_nhi = g.c_nhi;
+    G.c_nlo = g.c_nlo;
+    for (int q = 0; q < 4; ++q) G.ext[q] = D.ext[q];
+    G.gap = box_gap_exact(D.ext);
+}
+
+// One plane: damped Newton from (x, y, z) (z floored first) until converged,
+// given up, or max_iter iterations; returns the newton_iteration status.
+__device__ __forceinline__ int solve_plane(const NewtonGeom &G, const hhsar_geom &g, double tu,
+                                           double tv, double tn, double &x, double &y, double &z,
+                                           int &it) {
+    const double max_step2 = g.max_step * g.max_step;
+    if (z < g.z_floor) z = g.z_floor;
+    it = 0;
+    int st = 0;
+    while (st == 0 && it < g.max_iter) {
+        ++it;
+        st = newton_iteration(G, tu, tv, tn, x, y, z, g.tol, max_step2, g.max_step, g.z_floor);
+    }
+    return st;
+}
+
+__device__ __forceinline__ double plane_target(const hhsar_grid_desc &D, const hhsar_geom &g,
+                                               int w) {
+    return xadd(D.origin[2], xmul(g.step, (double)w));
+}
+
+// Masks and counters of plane w of a column once its solve is final:
+// containment (slack) -> valid point, leaf delay window (ffbp.py:320-335),
+// core counts; positions of contained points.
+__device__ __forceinline__ void finish_plane(const hhsar_grid_desc &D, const hhsar_geom &g, int w,
+                                             bool ok, double x, double y, double z, bool core_uv,
+                                             int64_t base, uint8_t *__restrict__ valid,
+                                             double *__restrict__ positions, unsigned (&acc)[6]) {
+    if (w < D.near_lo[2]) return;
+    const bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] && y >= D.slack_lo[1] &&
+                     y <= D.slack_hi[1] && z >= D.slack_lo[2] && z <= D.slack_hi[2];
+    bool post = pre;
+    if (pre && D.is_leaf) {
+        // 2 * max corner distance / c <= window_hi (ffbp.py:320-330).  The
+        // farthest of the 8 corners takes, per axis, the bound farther from
+        // the point; rounded subtraction, squaring, addition and sqrt are all
+        // monotone, so its rounded distance IS the reference's max over the 8
+        // (bit-exact, 1 sqrt not 8).
+        const double ex0 = xsub(x, D.box[0]), ex1 = xsub(x, D.box[3]);
+        const double ey0 = xsub(y, D.box[1]), ey1 = xsub(y, D.box[4]);
+        const double ez0 = xsub(z, D.box[2]), ez1 = xsub(z, D.box[5]);
+        const double fx = fabs(ex0) >= fabs(ex1) ? ex0 : ex1;
+        const double fy = fabs(ey0) >= fabs(ey1) ? ey0 : ey1;
+        const double fz = fabs(ez0) >= fabs(ez1) ? ez0 : ez1;
+        const double dmax = xsqrt(xadd(xadd(xsq(fx), xsq(fy)), xsq(fz)));
+        post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
+    }
+    const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
+    acc[0] += pre;
+    acc[1] += pre && in_core;
+    acc[2] += post;
+    acc[3] += post && in_core;
+    if (post) valid[base + w] = 1;
+    if (pre) {
+        double *pp = positions + 3 * (base + w);
+        pp[0] = x;
+        pp[1] = y;
+        pp[2] = z;
+    }
+}
+
+__device__ __forceinline__ void flush_stats(int64_t *__restrict__ stats, int gi,
+                                            unsigned (&acc)[6]) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        if (acc[q])
+            atomicAdd((unsigned long long *)(stats + (int64_t)gi * HHSAR_GRID_STATS + q),
+                      (unsigned long long)acc[q]);
+        acc[q] = 0;
+    }
+}
+
+// Heavy columns -- (u, v) outside the far-field ellipse (tu/U)^2 + (tv/V)^2
+// < 1, U = c_uv dx, V = c_uv dy -- fail plane after plane (config 3: 6% of
+// the columns, ~800 iterations each against ~80, 39% of all iterations), and
+// a failed plane restarts the next one from the region centre, so their
+// chains are mostly broken.  grid_newton_heavy_list_kernel collects them;
+// grid_newton_kernel solves every heavy plane independently from the centre
+// (one task per plane, started before the light columns) and stores the
+// speculative (ok, iterations) in `valid`, positions in `positions`;
+// grid_newton_fixup_kernel then walks each heavy column in the reference's
+// order and re-solves, warm-started, exactly the planes whose predecessor
+// converged (the reference did not restart those from the centre).  Every
+// plane ends with the reference's start point, so results and iteration
+// counts are unchanged; all tasks are short, so the persistent kernel can
+// run at full occupancy without a long tail.
+__device__ __forceinline__ uint8_t spec_code(bool ok, int it) {
+    return (uint8_t)((ok ? 0x80 : 0) | (it & 0x7f));  // it <= max_iter <= 127
+}
+
+__global__ void grid_newton_heavy_list_kernel(const hhsar_grid_desc *__restrict__ grids,
+                                              int n_grids, int64_t n_cols,
+                                              const int32_t *__restrict__ block_grid,
+                                              hhsar_geom g, int32_t *__restrict__ heavy,
+                                              unsigned long long *__restrict__ n_heavy) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool h = false;
+    if (c < n_cols) {
+        const Column q = decode_column(grids, n_grids, block_grid, g, (unsigned long long)c);
+        h = column_is_heavy(grids[q.gi], g, q.tu, q.tv);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, h);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long b0 = 0;
+    if (lane == __ffs(m) - 1) b0 = atomicAdd(n_heavy, (unsigned long long)__popc(m));
+    b0 = __shfl_sync(0xffffffffu, b0, __ffs(m) - 1);
+    if (h) heavy[b0 + __popc(m & ((1u << lane) - 1u))] = (int32_t)c;
+}
 
 __global__ void __launch_bounds__(NEWTON_THREADS)
 grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
                    const int32_t *__restrict__ block_grid, hhsar_geom g,
                    double *__restrict__ positions, uint8_t *__restrict__ valid,
-                   int64_t *__restrict__ stats, unsigned long long *__restrict__ counter) {
-    const double max_step2 = g.max_step * g.max_step;
+                   int64_t *__restrict__ stats, unsigned long long *__restrict__ counter,
+                   const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ n_heavy_p) {
     NewtonGeom G;
-    G.c_uv = g.c_uv;
-    G.c_nhi = g.c_nhi;
-    G.c_nlo = g.c_nlo;
     int gi = -1, acc_gi = -1, w = 0, w_end = 0, it = 0, iu = 0, iv = 0;
     int64_t base = 0;  // lattice index of plane 0 of the current column
-    bool have = false, core_uv = false;
+    bool have = false, core_uv = false, spec = false;
     double tu = 0, tv = 0, tn = 0, x = 0, y = 0, z = 0;
+    const double max_step2 = g.max_step * g.max_step;
+    const unsigned long long n_spec = *n_heavy_p * HEAVY_MAXP;  // heavy (column, plane) slots
     unsigned acc[6] = {0, 0, 0, 0, 0, 0};
-    auto flush = [&]() {
-        if (acc_gi < 0) return;
-        int64_t *st = stats + (int64_t)acc_gi * HHSAR_GRID_STATS;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            if (acc[q]) atomicAdd((unsigned long long *)(st + q), (unsigned long long)acc[q]);
-            acc[q] = 0;
-        }
-    };
     auto start_plane = [&](const hhsar_grid_desc &D, double sx, double sy, double sz) {
-        tn = xadd(D.origin[2], xmul(g.step, (double)w));
+        tn = plane_target(D, g, w);
         x = sx;
         y = sy;
         z = sz > g.z_floor ? sz : g.z_floor;
@@ -318,40 +476,38 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
     };
     while (true) {
         if (!have) {
-            const unsigned long long c = atomicAdd(counter, 1ull);
-            if (c >= (unsigned long long)n_cols) break;
-            int g2;
-            if (block_grid) {
-                g2 = block_grid[c >> 7];
-                while (g2 + 1 < n_grids && (unsigned long long)grids[g2 + 1].col_offset <= c) ++g2;
-            } else {  // last grid whose col_offset <= c (empty grids share the next offset)
-                int lo = 0, hi = n_grids - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if ((unsigned long long)grids[mid].col_offset <= c) lo = mid; else hi = mid - 1;
+            // first the heavy planes (one task each), then the light columns
+            const unsigned long long t = atomicAdd(counter, 1ull);
+            if (t >= n_spec + (unsigned long long)n_cols) break;
+            spec = t < n_spec;
+            const unsigned long long c =
+                spec ? (unsigned long long)heavy[t / HEAVY_MAXP] : t - n_spec;
+            const Column q = decode_column(grids, n_grids, block_grid, g, c);
+            const hhsar_grid_desc &D = grids[q.gi];
+            const int wend_col = D.near_hi[2] + 1;
+            if (spec) {
+                w = (int)(t % HEAVY_MAXP);
+                if (w >= wend_col) continue;
+                w_end = w + 1;
+            } else {
+                if (column_is_heavy(D, g, q.tu, q.tv)) continue;
+                w = 0;
+                w_end = wend_col;
+                if (q.gi != acc_gi) {
+                    if (acc_gi >= 0) flush_stats(stats, acc_gi, acc);
+                    acc_gi = q.gi;
                 }
-                g2 = lo;
             }
-            if (g2 != acc_gi) {
-                flush();
-                acc_gi = g2;
-            }
-            gi = g2;
-            const hhsar_grid_desc &D = grids[gi];
-            const int64_t k = (int64_t)c - D.col_offset;
-            const int wv = D.act_hi[1] - D.act_lo[1] + 1;
-            iu = D.act_lo[0] + (int)(k / wv);
-            iv = D.act_lo[1] + (int)(k % wv);
+            gi = q.gi;
+            iu = q.iu;
+            iv = q.iv;
+            tu = q.tu;
+            tv = q.tv;
             base = D.offset + ((int64_t)iu * D.dims[1] + iv) * D.dims[2];
-            tu = xadd(D.origin[0], xmul(g.step, (double)iu));
-            tv = xadd(D.origin[1], xmul(g.step, (double)iv));
             core_uv = iu >= D.core_lo[0] && iu <= D.core_hi[0] && iv >= D.core_lo[1] &&
                       iv <= D.core_hi[1];
-            w_end = D.near_hi[2] + 1;
-            for (int q = 0; q < 4; ++q) G.ext[q] = D.ext[q];
-            G.gap = box_gap_exact(D.ext);
-            w = 0;
-            have = w_end > 0;
+            column_geom(D, g, G);
+            have = w < w_end;
             if (have) start_plane(D, g.center[0], g.center[1], g.center[2]);
             continue;
         }
@@ -362,41 +518,18 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         // plane w finished: masks, counters, warm start for plane w + 1
         const hhsar_grid_desc &D = grids[gi];
         const bool ok = st == 1;
+        if (spec) {  // speculative: the fix-up kernel decides
+            valid[base + w] = spec_code(ok, it);
+            double *pp = positions + 3 * (base + w);
+            pp[0] = x;
+            pp[1] = y;
+            pp[2] = z;
+            have = false;
+            continue;
+        }
         acc[4] += it;
         acc[5] += 1;
-        if (w >= D.near_lo[2]) {
-            const bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] &&
-                             y >= D.slack_lo[1] && y <= D.slack_hi[1] && z >= D.slack_lo[2] &&
-                             z <= D.slack_hi[2];
-            bool post = pre;
-            if (pre && D.is_leaf) {
-                // 2 * max corner distance / c <= window_hi (ffbp.py:320-330).
-                // The farthest of the 8 corners takes, per axis, the bound
-                // farther from the point; rounded subtraction, squaring,
-                // addition and sqrt are all monotone, so its rounded distance
-                // IS the reference's max over the 8 (bit-exact, 1 sqrt not 8).
-                const double ex0 = xsub(x, D.box[0]), ex1 = xsub(x, D.box[3]);
-                const double ey0 = xsub(y, D.box[1]), ey1 = xsub(y, D.box[4]);
-                const double ez0 = xsub(z, D.box[2]), ez1 = xsub(z, D.box[5]);
-                const double fx = fabs(ex0) >= fabs(ex1) ? ex0 : ex1;
-                const double fy = fabs(ey0) >= fabs(ey1) ? ey0 : ey1;
-                const double fz = fabs(ez0) >= fabs(ez1) ? ez0 : ez1;
-                const double dmax = xsqrt(xadd(xadd(xsq(fx), xsq(fy)), xsq(fz)));
-                post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
-            }
-            const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
-            acc[0] += pre;
-            acc[1] += pre && in_core;
-            acc[2] += post;
-            acc[3] += post && in_core;
-            if (post) valid[base + w] = 1;
-            if (pre) {
-                double *pp = positions + 3 * (base + w);
-                pp[0] = x;
-                pp[1] = y;
-                pp[2] = z;
-            }
-        }
+        finish_plane(D, g, w, ok, x, y, z, core_uv, base, valid, positions, acc);
         ++w;
         if (w >= w_end) {
             have = false;
@@ -407,7 +540,56 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         else
             start_plane(D, g.center[0], g.center[1], g.center[2]);
     }
-    flush();
+    if (acc_gi >= 0) flush_stats(stats, acc_gi, acc);
+}
+
+__global__ void __launch_bounds__(NEWTON_THREADS)
+grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
+                         const int32_t *__restrict__ block_grid, hhsar_geom g,
+                         double *__restrict__ positions, uint8_t *__restrict__ valid,
+                         int64_t *__restrict__ stats, const int32_t *__restrict__ heavy,
+                         const unsigned long long *__restrict__ n_heavy_p) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)*n_heavy_p) return;
+    const Column q = decode_column(grids, n_grids, block_grid, g, (unsigned long long)heavy[i]);
+    const hhsar_grid_desc &D = grids[q.gi];
+    NewtonGeom G;
+    column_geom(D, g, G);
+    const int w_end = D.near_hi[2] + 1;
+    const int64_t base = D.offset + ((int64_t)q.iu * D.dims[1] + q.iv) * D.dims[2];
+    const bool core_uv = q.iu >= D.core_lo[0] && q.iu <= D.core_hi[0] && q.iv >= D.core_lo[1] &&
+                         q.iv <= D.core_hi[1];
+    unsigned acc[6] = {0, 0, 0, 0, 0, 0};
+    bool prev_ok = false;
+    double px = 0, py = 0, pz = 0;
+    for (int w = 0; w < w_end; ++w) {
+        const uint8_t code = valid[base + w];
+        double *pp = positions + 3 * (base + w);
+        bool ok;
+        int it;
+        double x, y, z;
+        if (!prev_ok) {  // the reference also started this plane from the centre
+            ok = code & 0x80;
+            it = code & 0x7f;
+            x = pp[0];
+            y = pp[1];
+            z = pp[2];
+        } else {  // warm start from the converged predecessor
+            x = px;
+            y = py;
+            z = pz;
+            ok = solve_plane(G, g, q.tu, q.tv, plane_target(D, g, w), x, y, z, it) == 1;
+        }
+        valid[base + w] = 0;  // clear the speculative code; finish_plane sets 1
+        acc[4] += it;
+        acc[5] += 1;
+        finish_plane(D, g, w, ok, x, y, z, core_uv, base, valid, positions, acc);
+        prev_ok = ok;
+        px = x;
+        py = y;
+        pz = z;
+    }
+    flush_stats(stats, q.gi, acc);
 }
 
 __global__ void invert_newton_kernel(NewtonGeom G, const double *__restrict__ t,
@@ -468,26 +650,25 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
                                                       0);
         if (per_sm <= 0) per_sm = 1;
     }
+    // scratch: [0] work counter, [1] heavy-column count, then the heavy list
     unsigned long long *counter = nullptr;
-    if (cudaMallocAsync(&counter, sizeof(unsigned long long), s) != cudaSuccess)
-        return set_error(HHSAR_ECUDA, "grid_newton: counter allocation failed");
-    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
-    // Lanes own whole columns (warm starts chain along n), so the kernel ends
-    // when the last long column does: keep ~COLS columns per lane for the
-    // balance, within [1, occupancy] CTAs per SM.
-    const char *cpl = getenv("HHSAR_NEWTON_CPL");  // experiment knob
-    const int64_t COLS = cpl ? atoi(cpl) : 4;
-    int64_t bps = (n_cols + COLS * NEWTON_THREADS * sm_count() / 2) /
-                  (COLS * NEWTON_THREADS * sm_count());  // whole CTAs per SM (even spread)
-    if (bps > per_sm) bps = per_sm;
-    if (bps < 1) bps = 1;
-    int64_t blocks = bps * sm_count();
-    const int64_t need = (n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS;
-    if (blocks > need) blocks = need;
+    if (cudaMallocAsync(&counter, 2 * sizeof(unsigned long long) + n_cols * sizeof(int32_t), s) !=
+        cudaSuccess)
+        return set_error(HHSAR_ECUDA, "grid_newton: scratch allocation failed");
+    cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), s);
+    int32_t *heavy = reinterpret_cast<int32_t *>(counter + 2);
+    grid_newton_heavy_list_kernel<<<(unsigned)((n_cols + 255) / 256), 256, 0, s>>>(
+        grids, (int)n_grids, n_cols, block_grid, *geom, heavy, counter + 1);
+    // every task is short (a heavy plane or a light column), so full occupancy
+    const int64_t blocks = (int64_t)sm_count() * per_sm;
     grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
-        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter);
+        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
+        counter + 1);
+    grid_newton_fixup_kernel<<<(unsigned)((n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS),
+                               NEWTON_THREADS, 0, s>>>(grids, (int)n_grids, block_grid, *geom,
+                                                       positions, valid, stats, heavy, counter + 1);
     cudaFreeAsync(counter, s);
-    return check_launch("grid_newton_kernel");
+    return check_launch("grid_newton_kernel / grid_newton_fixup_kernel");
 }
 
 extern "C" int hhsar_invert_newton(const double *ext4, double k_min, double k_max,
