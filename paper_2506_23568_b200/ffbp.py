@@ -200,6 +200,37 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     return finish_lattices(pending, newton_grids)
 
 
+_PLAN_UPLOADS = {}
+
+
+def _plan_upload(sched: Schedule, region):
+    """Pinned host image of the plan's inputs -- grid descriptors | leaf
+    bounds | boundary lattice | status word (8-byte aligned pieces) -- built
+    once per (schedule, region) and reused: its content never changes and
+    the device copy is taken asynchronously from it."""
+    import torch
+    key = (id(sched), sched.n_grids, tuple(float(v) for v in _region_tuple(region)))
+    hit = _PLAN_UPLOADS.get(key)
+    if hit is not None and hit[3] is sched:
+        return hit[:3]
+    bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
+    parts = [sched.grids.view(np.uint8).reshape(-1), sched.bounds.astype(np.int64).view(np.uint8),
+             bl.view(np.uint8).reshape(-1), np.zeros(8, dtype=np.uint8)]
+    cuts = np.cumsum([0] + [p.size for p in parts])
+    staged = torch.empty(int(cuts[-1]), dtype=torch.uint8, pin_memory=True)
+    sn = staged.numpy()
+    for p, a in zip(parts, cuts[:-1]):
+        sn[a:a + p.size] = p
+    if len(_PLAN_UPLOADS) > 8:
+        _PLAN_UPLOADS.clear()
+    _PLAN_UPLOADS[key] = (staged, cuts, bl.shape[0], sched)
+    return staged, cuts, bl.shape[0]
+
+
+def _region_tuple(region):
+    return (region.x_min, region.x_max, region.y_min, region.y_max, region.z_min, region.z_max)
+
+
 def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float, pad: int,
                   window_hi: float, tol: float = 1e-9, max_iter: int = 50):
     """Launch the leaf boxes + plan kernels and the asynchronous readback of
@@ -208,16 +239,7 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     import torch
     dev = el_dev.device
     stream = _native.stream_handle()
-    bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
-    # one pinned, asynchronous upload: grid descriptors | leaf bounds |
-    # boundary lattice | status word (all 8-byte aligned pieces)
-    parts = [sched.grids.view(np.uint8).reshape(-1), sched.bounds.astype(np.int64).view(np.uint8),
-             bl.view(np.uint8).reshape(-1), np.zeros(8, dtype=np.uint8)]
-    cuts = np.cumsum([0] + [p.size for p in parts])
-    staged = torch.empty(int(cuts[-1]), dtype=torch.uint8, pin_memory=True)
-    sn = staged.numpy()
-    for p, a in zip(parts, cuts[:-1]):
-        sn[a:a + p.size] = p
+    staged, cuts, n_b = _plan_upload(sched, region)
     up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
     up.copy_(staged, non_blocking=True)
     descs_dev = up[cuts[0]:cuts[1]]
@@ -229,8 +251,7 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
                  _native.ptr(leaf_box), stream)
     geom = make_geom(region, kgrid, gamma, margin, pad, window_hi, tol, max_iter)
     _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
-                 _native.ptr(boundary), bl.shape[0], _native.ptr(geom), _native.ptr(status),
-                 stream)
+                 _native.ptr(boundary), n_b, _native.ptr(geom), _native.ptr(status), stream)
     back = torch.empty(int(cuts[1]) + 8, dtype=torch.uint8, pin_memory=True)
     back[:cuts[1]].copy_(descs_dev, non_blocking=True)
     back[cuts[1]:].copy_(status, non_blocking=True)
@@ -238,7 +259,7 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     done.record()
     return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
                 host_d=back[:cuts[1]], host_s=back[cuts[1]:cuts[1] + 4].view(torch.int32),
-                done=done, keep=(staged, up, leaf_box))
+                done=done, back=back, keep=(staged, up, leaf_box))
 
 
 _trace = None  # optional host-timeline hook (tools/host_overhead.py)
@@ -274,12 +295,13 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     host["col_offset"][1:] = starts[:-1]
     if _trace:
         _trace("worklist built")
-    # descriptors go back up through the plan's pinned staging buffer (its
-    # upload completed before the plan ran) into the plan's device copy
-    staged, up = p["keep"][0], p["keep"][1]
+    # descriptors go back up through the plan's pinned read-back buffer (its
+    # D2H copy completed: we synchronised on it) into the plan's device copy
+    back, up = p["back"], p["keep"][1]
     nb = host.nbytes
-    staged.numpy()[:nb] = host.view(np.uint8).reshape(-1)
-    up[:nb].copy_(staged[:nb], non_blocking=True)
+    back.numpy()[:nb] = host.view(np.uint8).reshape(-1)
+    up[:nb].copy_(back[:nb], non_blocking=True)
+    staged = back
     descs_dev = up[:nb]
     if _trace:
         _trace("descs uploaded")
@@ -439,13 +461,13 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     main = torch.cuda.current_stream()
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
-    # range compression first: it needs no host preparation and hides the
-    # schedule / plan set-up below
-    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
+    # the (cached) plan set-up is launched first on the high-priority stream,
+    # then the range compression; the host waits only for the plan
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)
+    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
     with torch.cuda.stream(geo):
         lat = finish_lattices(pending)
     main.wait_stream(geo)
