@@ -274,7 +274,9 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     sched, descs_dev, geom = p["sched"], p["descs_dev"], p["geom"]
     dev = descs_dev.device
     stream = _native.stream_handle()
-    host = p["host_d"].numpy().copy().view(_native.GRID_DTYPE)  # byte copy, then the record view
+    # the plan's pinned read-back IS the host descriptor table from here on
+    # (edited in place, uploaded from, kept alive with the lattices)
+    host = p["host_d"].numpy().view(_native.GRID_DTYPE)
     if int(p["host_s"][0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
     dims = host["dims"].astype(np.int64)
@@ -299,7 +301,6 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     # D2H copy completed: we synchronised on it) into the plan's device copy
     back, up = p["back"], p["keep"][1]
     nb = host.nbytes
-    back.numpy()[:nb] = host.view(np.uint8).reshape(-1)
     up[:nb].copy_(back[:nb], non_blocking=True)
     staged = back
     descs_dev = up[:nb]
