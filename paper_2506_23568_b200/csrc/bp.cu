@@ -95,7 +95,7 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
                 int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el, int m,
                 const float2 *__restrict__ env, BpFast k, float2 *__restrict__ out,
                 int64_t *__restrict__ oow_total, int tx_base, int n_tiles, int split,
-                float2 *__restrict__ part) {
+                float2 *__restrict__ part, const float2 *__restrict__ rot) {
     constexpr int TL_VX = VX;  // voxels per thread along x
     __shared__ float4 s_env[TL_CHUNK * TL_W];  // 32 KB
     __shared__ float4 s_el[TL_CHUNK];          // x, y, z, bits(byte offset | -1 = slow)
@@ -172,8 +172,10 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
             const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
             const float2 v0 = __ldg(row + min(bin, k.n_t - 1));
             const float2 v1 = __ldg(row + min(bin + 1, k.n_t - 1));
-            // pre-rotate by the carrier at the bin: k_ref c (t0 + bin dt), float64
-            const float2 r = cis_reduced(k.kc_t0 + k.alpha_d * (double)bin);
+            // pre-rotate by the carrier at the bin: exp(j k_ref c (t0 + bin dt)),
+            // float64 phase rounded once, from the per-launch table (keeps the
+            // staging's sincos and conversions off the SFU the units saturate)
+            const float2 r = __ldg(rot + bin);
             const float2 dv = bin < k.n_t - 1 ? make_float2(v1.x - v0.x, v1.y - v0.y)
                                               : make_float2(0.f, 0.f);
             const float2 a = cmul(v0, r), b2 = cmul(dv, r);
@@ -411,6 +413,13 @@ int tile_split(int64_t tiles, int64_t m, int per_sm) {
     return best;
 }
 
+// exp(j k_ref c (t0 + dt bin)) per delay bin (float64 phase, reduced, then
+// the fp32 sincos), shared by every element's window staging
+__global__ void bp_rot_kernel(float2 *__restrict__ rot, int n_t, double kc_t0, double alpha_d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_t) rot[i] = cis_reduced(kc_t0 + alpha_d * (double)i);
+}
+
 struct TileArgs {
     const double *origin, *step;
     int nx, ny, nz;
@@ -421,6 +430,7 @@ struct TileArgs {
     BpFast k;
     float2 *out;
     int64_t *oow;
+    const float2 *rot;
     cudaStream_t s;
 };
 
@@ -446,7 +456,7 @@ int launch_tile(const TileArgs &a) {
         return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
     bpa_tile_kernel<VX, MINB, PAIR><<<(unsigned)(tiles * split), TL_THREADS, 0, a.s>>>(
         a.origin[0], a.origin[1], a.origin[2], a.step[0], a.step[1], a.step[2], a.nx, a.ny, a.nz,
-        a.vb, a.ve, a.el, a.m, a.env, a.k, a.out, a.oow, tx0, (int)tiles, split, part);
+        a.vb, a.ve, a.el, a.m, a.env, a.k, a.out, a.oow, tx0, (int)tiles, split, part, a.rot);
     if (split > 1) {
         add_parts_kernel<<<4 * sm_count(), 256, 0, a.s>>>(a.out, part, split - 1, nv);
         cudaFreeAsync(part, a.s);
@@ -507,19 +517,27 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
             const char *v = getenv("HHSAR_BPA_VARIANT");
             return v ? atoi(v) : 0;
         }();
+        float2 *rot = nullptr;
+        if (cudaMallocAsync(&rot, n_t * sizeof(float2), s) != cudaSuccess)
+            return set_error(HHSAR_ECUDA, "bpa_cartesian: table allocation failed");
+        bp_rot_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(rot, (int)n_t, k.kc_t0,
+                                                                    k.alpha_d);
         const TileArgs a{origin, step, nx, ny, nz, vox_begin, vox_end,
                          reinterpret_cast<const float4 *>(el_xyz), (int)m,
                          reinterpret_cast<const float2 *>(envelopes), k,
-                         reinterpret_cast<float2 *>(out), oow_total, s};
+                         reinterpret_cast<float2 *>(out), oow_total, rot, s};
+        int rc;
         switch (variant) {
             // A/B variants (HHSAR_BPA_VARIANT): VX voxels/thread, min CTAs/SM,
             // packed fp32x2 pair path.  Default measured fastest on B200.
-            case 1: return launch_tile<4, 5, false>(a);
-            case 2: return launch_tile<8, 3, false>(a);
-            case 3: return launch_tile<8, 3, true>(a);
-            case 4: return launch_tile<4, 4, true>(a);
-            default: return launch_tile<4, 5, true>(a);
+            case 1: rc = launch_tile<4, 5, false>(a); break;
+            case 2: rc = launch_tile<8, 3, false>(a); break;
+            case 3: rc = launch_tile<8, 3, true>(a); break;
+            case 4: rc = launch_tile<4, 4, true>(a); break;
+            default: rc = launch_tile<4, 5, true>(a); break;
         }
+        cudaFreeAsync(rot, s);
+        return rc;
     }
     const int64_t tiles = (int64_t)((nx + CART_V - 1) / CART_V) * ((ny + CART_TY - 1) / CART_TY) *
                           ((nz + CART_TZ - 1) / CART_TZ);
