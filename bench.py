@@ -278,6 +278,7 @@ def run_ours(args):
             free, _ = torch.cuda.mem_get_info(dev)
             if free > 120e9:  # config 4: 17 GB cube + 69 GB profiles + lattices
                 result["hhffbpa"]["config4"] = hhffbpa_leg(4, dev, min(args.steps, 3))
+            result["hhffbpa"]["config2_leaf_sweep"] = leaf_sweep_leg(dev, args.steps)
             check = hhffbpa_leg(2, dev, 1, check=True)
             for k in ("parity_vs_oracle", "cpu_oracle_s", "cpu_oracle_cores"):
                 result["hhffbpa"]["config2"][k] = check[k]
@@ -315,6 +316,50 @@ def metrics_leg(volume, dims):
             "psnr_gbs": round(4 * 8 * n / ps / 1e6, 1), "mip_ms": round(mp, 3),
             "mip_gbs": round(8 * n / mp / 1e6, 1), "hbm_peak_gbs": hbm,
             "note": "host wall time per call incl. two scalar read-backs (psnr)"}
+
+
+def leaf_sweep_leg(dev, steps):
+    """BASELINE config 2's sweep: HHFFBPA with merge factor 4 and leaves of
+    8 / 16 / 32 frames (2^(M-1) balanced leaves of the 4,000 x 8 element
+    aperture, M = 10 / 9 / 8), each against direct BPA on the same cube:
+    device time per volume, complex rel-L2 and PSNR (GPU metrics) vs BPA."""
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, ffbp, metrics, rangecomp, workloads
+    w = workloads.config(2)
+    cube = _native.simulate(np.asarray(w.aperture.elements), w.scene_pos, w.scene_refl,
+                            w.freqs.k_samples, device=dev)
+    el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+    el4 = bpa.el_f32x4(el)
+    env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
+    ref, _ = bpa.bpa_volume_device(env, el4, w.region, w.dims, 0.0, dt, k_ref)
+    torch.cuda.synchronize()
+    out = {"workload": "BASELINE config 2 sweep: merge factor 4, leaves of 8/16/32 frames "
+                       "(M = 10/9/8), accuracy against direct BPA on the same cube"}
+    for frames, levels in ((8, 10), (16, 9), (32, 8)):
+        params = ffbp.FfbpParams(levels=levels)
+
+        def step():
+            return ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params,
+                                          levels, 4, w.upsample)
+        for _ in range(3):
+            run = step()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            run = step()
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        v = run.volume
+        out[f"leaf_{frames}_frames"] = {
+            "levels": levels, "leaf_elements": int(w.n_elements // 2 ** (levels - 1)),
+            "ms_per_step": round(ms, 3), "volumes_per_s": round(1e3 / ms, 1),
+            "rel_l2_vs_bpa": round((torch.linalg.norm(v - ref) / torch.linalg.norm(ref)).item(), 4),
+            "psnr_vs_bpa_db": round(metrics.psnr_device(ref, v), 2)}
+    del cube, env, ref
+    torch.cuda.empty_cache()
+    return out
 
 
 def hhffbpa_leg(index, dev, steps, check=False):
