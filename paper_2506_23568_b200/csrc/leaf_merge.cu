@@ -190,6 +190,7 @@ __device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, co
     float2 acc = make_float2(0.f, 0.f);
     if (KERNEL == 0) {
         const float2 *b = base + ((iu * C.nv + iv) * C.nn + iw);
+        f2x a2 = pk2(0.f, 0.f);  // (re, im) accumulated with FFMA2, scalar weights broadcast
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
             const float wa = a ? fu : 1.f - fu;
@@ -199,10 +200,11 @@ __device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, co
                 const float2 *row = b + a * su + bb * C.nn;
                 const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
                 const float w0 = wa * wb * (1.f - fn), w1 = wa * wb * fn;
-                acc.x = fmaf(v0.x, w0, fmaf(v1.x, w1, acc.x));
-                acc.y = fmaf(v0.y, w0, fmaf(v1.y, w1, acc.y));
+                a2 = fma2(pk2(v1.x, v1.y), bc2(w1), a2);
+                a2 = fma2(pk2(v0.x, v0.y), bc2(w0), a2);
             }
         }
+        acc = make_float2(lo2(a2), hi2(a2));
     } else {
         float wu[4], wv[4], wn[4];
         keys_weights(fu, wu);
