@@ -458,14 +458,17 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                    const int32_t *__restrict__ block_grid, hhsar_geom g,
                    double *__restrict__ positions, uint8_t *__restrict__ valid,
                    int64_t *__restrict__ stats, unsigned long long *__restrict__ counter,
-                   const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ n_heavy_p) {
+                   const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ n_heavy_p,
+                   int phase) {
     NewtonGeom G;
     int gi = -1, acc_gi = -1, w = 0, w_end = 0, it = 0, iu = 0, iv = 0;
     int64_t base = 0;  // lattice index of plane 0 of the current column
     bool have = false, core_uv = false, spec = false;
     double tu = 0, tv = 0, tn = 0, x = 0, y = 0, z = 0;
     const double max_step2 = g.max_step * g.max_step;
-    const unsigned long long n_spec = *n_heavy_p * HEAVY_MAXP;  // heavy (column, plane) slots
+    // phase 0: heavy (column, plane) slots only; phase 1: light columns only
+    const unsigned long long n_spec = phase == 0 ? *n_heavy_p * HEAVY_MAXP : 0;
+    const unsigned long long n_light = phase == 0 ? 0 : (unsigned long long)n_cols;
     unsigned acc[6] = {0, 0, 0, 0, 0, 0};
     auto start_plane = [&](const hhsar_grid_desc &D, double sx, double sy, double sz) {
         tn = plane_target(D, g, w);
@@ -478,7 +481,7 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         if (!have) {
             // first the heavy planes (one task each), then the light columns
             const unsigned long long t = atomicAdd(counter, 1ull);
-            if (t >= n_spec + (unsigned long long)n_cols) break;
+            if (t >= n_spec + n_light) break;
             spec = t < n_spec;
             const unsigned long long c =
                 spec ? (unsigned long long)heavy[t / HEAVY_MAXP] : t - n_spec;
@@ -659,14 +662,34 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     int32_t *heavy = reinterpret_cast<int32_t *>(counter + 2);
     grid_newton_heavy_list_kernel<<<(unsigned)((n_cols + 255) / 256), 256, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, heavy, counter + 1);
-    // every task is short (a heavy plane or a light column), so full occupancy
+    // every task is short (a heavy plane or a light column), so full occupancy.
+    // 1. heavy planes; 2. the light columns on `s` while the latency-bound
+    // in-order fix-up of the heavy columns runs beside them on a side stream
     const int64_t blocks = (int64_t)sm_count() * per_sm;
     grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
-        counter + 1);
+        counter + 1, 0);
+    static cudaStream_t side = nullptr;
+    static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    if (!side) {
+        int lo = 0, hi = 0;  // the fix-up must not queue behind range-compression CTAs
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
+        cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+    }
+    cudaEventRecord(fork_ev, s);
+    cudaStreamWaitEvent(side, fork_ev, 0);
     grid_newton_fixup_kernel<<<(unsigned)((n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS),
-                               NEWTON_THREADS, 0, s>>>(grids, (int)n_grids, block_grid, *geom,
-                                                       positions, valid, stats, heavy, counter + 1);
+                               NEWTON_THREADS, 0, side>>>(grids, (int)n_grids, block_grid, *geom,
+                                                          positions, valid, stats, heavy,
+                                                          counter + 1);
+    cudaEventRecord(join_ev, side);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);  // work counter for phase 1
+    grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
+        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
+        counter + 1, 1);
+    cudaStreamWaitEvent(s, join_ev, 0);
     cudaFreeAsync(counter, s);
     return check_launch("grid_newton_kernel / grid_newton_fixup_kernel");
 }
