@@ -262,7 +262,7 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
                        const uint8_t *valid, const float4 *el, const float2 *env, int64_t n_t,
                        double t0, double dt, double k_ref, const hhsar_geom &g, int downconvert,
                        float2 *values, int64_t *oow_total, cudaStream_t s) {
-    constexpr int P = 4;
+    constexpr int P = 2;  // 512-point chunks: finer fill and 40 registers (P = 4: +8% at config 4)
     LeafFast k;
     k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
     k.x0 = (float)(t0 / dt);
