@@ -311,11 +311,11 @@ struct Column {
     double tu, tv;
 };
 
-__device__ __forceinline__ Column decode_column(const hhsar_grid_desc *__restrict__ grids,
-                                                int n_grids, const int32_t *block_grid,
-                                                const hhsar_geom &g, unsigned long long c) {
+__device__ __forceinline__ Column decode_in_grid(const hhsar_grid_desc *__restrict__ grids,
+                                                 int gi, const hhsar_geom &g,
+                                                 unsigned long long c) {
     Column q;
-    q.gi = grid_of_column(grids, n_grids, block_grid, c);
+    q.gi = gi;
     const hhsar_grid_desc &D = grids[q.gi];
     const int k = (int)((int64_t)c - D.col_offset);
     const int wv = D.act_hi[1] - D.act_lo[1] + 1;
@@ -326,6 +326,16 @@ __device__ __forceinline__ Column decode_column(const hhsar_grid_desc *__restric
     q.tv = xadd(D.origin[1], xmul(g.step, (double)q.iv));
     return q;
 }
+
+__device__ __forceinline__ Column decode_column(const hhsar_grid_desc *__restrict__ grids,
+                                                int n_grids, const int32_t *block_grid,
+                                                const hhsar_geom &g, unsigned long long c) {
+    return decode_in_grid(grids, grid_of_column(grids, n_grids, block_grid, c), g, c);
+}
+
+// per-column record written once by grid_newton_heavy_list_kernel: the
+// column's grid index, bit 31 = heavy
+constexpr int32_t HEAVY_BIT = (int32_t)0x80000000;
 
 __device__ __forceinline__ bool column_is_heavy(const hhsar_grid_desc &D, const hhsar_geom &g,
                                                 double tu, double tv) {
@@ -437,12 +447,14 @@ __global__ void grid_newton_heavy_list_kernel(const hhsar_grid_desc *__restrict_
                                               int n_grids, int64_t n_cols,
                                               const int32_t *__restrict__ block_grid,
                                               hhsar_geom g, int32_t *__restrict__ heavy,
-                                              unsigned long long *__restrict__ n_heavy) {
+                                              unsigned long long *__restrict__ n_heavy,
+                                              int32_t *__restrict__ col_grid) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool h = false;
     if (c < n_cols) {
         const Column q = decode_column(grids, n_grids, block_grid, g, (unsigned long long)c);
         h = column_is_heavy(grids[q.gi], g, q.tu, q.tv);
+        col_grid[c] = q.gi | (h ? HEAVY_BIT : 0);
     }
     const unsigned m = __ballot_sync(0xffffffffu, h);
     if (!m) return;
@@ -459,7 +471,7 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                    double *__restrict__ positions, uint8_t *__restrict__ valid,
                    int64_t *__restrict__ stats, unsigned long long *__restrict__ counter,
                    const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ n_heavy_p,
-                   int phase) {
+                   int phase, const int32_t *__restrict__ col_grid) {
     NewtonGeom G;
     int gi = -1, acc_gi = -1, w = 0, w_end = 0, it = 0, iu = 0, iv = 0;
     int64_t base = 0;  // lattice index of plane 0 of the current column
@@ -485,7 +497,9 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
             spec = t < n_spec;
             const unsigned long long c =
                 spec ? (unsigned long long)heavy[t / HEAVY_MAXP] : t - n_spec;
-            const Column q = decode_column(grids, n_grids, block_grid, g, c);
+            const int32_t rec = __ldg(col_grid + c);
+            if (!spec && (rec & HEAVY_BIT)) continue;  // solved plane by plane in phase 0
+            const Column q = decode_in_grid(grids, rec & ~HEAVY_BIT, g, c);
             const hhsar_grid_desc &D = grids[q.gi];
             const int wend_col = D.near_hi[2] + 1;
             if (spec) {
@@ -493,7 +507,6 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                 if (w >= wend_col) continue;
                 w_end = w + 1;
             } else {
-                if (column_is_heavy(D, g, q.tu, q.tv)) continue;
                 w = 0;
                 w_end = wend_col;
                 if (q.gi != acc_gi) {
@@ -551,10 +564,12 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
                          const int32_t *__restrict__ block_grid, hhsar_geom g,
                          double *__restrict__ positions, uint8_t *__restrict__ valid,
                          int64_t *__restrict__ stats, const int32_t *__restrict__ heavy,
-                         const unsigned long long *__restrict__ n_heavy_p) {
+                         const unsigned long long *__restrict__ n_heavy_p,
+                         const int32_t *__restrict__ col_grid) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)*n_heavy_p) return;
-    const Column q = decode_column(grids, n_grids, block_grid, g, (unsigned long long)heavy[i]);
+    const unsigned long long c = (unsigned long long)heavy[i];
+    const Column q = decode_in_grid(grids, __ldg(col_grid + c) & ~HEAVY_BIT, g, c);
     const hhsar_grid_desc &D = grids[q.gi];
     NewtonGeom G;
     column_geom(D, g, G);
@@ -655,20 +670,21 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     }
     // scratch: [0] work counter, [1] heavy-column count, then the heavy list
     unsigned long long *counter = nullptr;
-    if (cudaMallocAsync(&counter, 2 * sizeof(unsigned long long) + n_cols * sizeof(int32_t), s) !=
-        cudaSuccess)
+    if (cudaMallocAsync(&counter, 2 * sizeof(unsigned long long) + 2 * n_cols * sizeof(int32_t),
+                        s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "grid_newton: scratch allocation failed");
     cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), s);
     int32_t *heavy = reinterpret_cast<int32_t *>(counter + 2);
+    int32_t *col_grid = heavy + n_cols;
     grid_newton_heavy_list_kernel<<<(unsigned)((n_cols + 255) / 256), 256, 0, s>>>(
-        grids, (int)n_grids, n_cols, block_grid, *geom, heavy, counter + 1);
+        grids, (int)n_grids, n_cols, block_grid, *geom, heavy, counter + 1, col_grid);
     // every task is short (a heavy plane or a light column), so full occupancy.
     // 1. heavy planes; 2. the light columns on `s` while the latency-bound
     // in-order fix-up of the heavy columns runs beside them on a side stream
     const int64_t blocks = (int64_t)sm_count() * per_sm;
     grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
-        counter + 1, 0);
+        counter + 1, 0, col_grid);
     static cudaStream_t side = nullptr;
     static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     if (!side) {
@@ -683,12 +699,12 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     grid_newton_fixup_kernel<<<(unsigned)((n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS),
                                NEWTON_THREADS, 0, side>>>(grids, (int)n_grids, block_grid, *geom,
                                                           positions, valid, stats, heavy,
-                                                          counter + 1);
+                                                          counter + 1, col_grid);
     cudaEventRecord(join_ev, side);
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);  // work counter for phase 1
     grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
-        counter + 1, 1);
+        counter + 1, 1, col_grid);
     cudaStreamWaitEvent(s, join_ev, 0);
     cudaFreeAsync(counter, s);
     return check_launch("grid_newton_kernel / grid_newton_fixup_kernel");
