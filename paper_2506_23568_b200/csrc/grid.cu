@@ -397,8 +397,19 @@ __device__ __forceinline__ void finish_plane(const hhsar_grid_desc &D, const hhs
         const double fx = fabs(ex0) >= fabs(ex1) ? ex0 : ex1;
         const double fy = fabs(ey0) >= fabs(ey1) ? ey0 : ey1;
         const double fz = fabs(ez0) >= fabs(ez1) ? ez0 : ez1;
-        const double dmax = xsqrt(xadd(xadd(xsq(fx), xsq(fy)), xsq(fz)));
-        post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
+        const double s2 = xadd(xadd(xsq(fx), xsq(fy)), xsq(fz));
+        // decided on the square unless within 1e-12 of the limit (the exact
+        // sqrt / divide round to < 3e-16 relative, so outside that band the
+        // reference's comparison cannot come out differently)
+        const double lim = 0.5 * HHSAR_C_LIGHT * g.window_hi, lim2 = lim * lim;
+        if (s2 < lim2 * (1.0 - 1e-12)) {
+            post = true;
+        } else if (s2 > lim2 * (1.0 + 1e-12)) {
+            post = false;
+        } else {
+            const double dmax = xsqrt(s2);
+            post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
+        }
     }
     const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
     acc[0] += pre;
