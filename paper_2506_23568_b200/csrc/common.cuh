@@ -96,7 +96,14 @@ __device__ __forceinline__ double rcp_d(double a) {
     return fma(y, fma(-a, y, 1.0), y);
 }
 
-__device__ __forceinline__ double sqrt_d(double a) { return a * rsqrt_d(a); }
+// sqrt by one Heron step from the SFU rsqrt seed y: s0 = a y, s = s0 +
+// (a - s0^2) y / 2 -- 4 float64 instructions, relative error ~2e-14
+__device__ __forceinline__ double sqrt_d(double a) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    const double s0 = a * y;
+    return fma(0.5 * y, fma(-s0, s0, a), s0);
+}
 
 // ---- fast float64 geometry for the merge stages ------------------------------
 // Same formulas, FMA allowed (not on a bit-exactness path).
