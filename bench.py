@@ -322,6 +322,35 @@ def metrics_leg(volume, dims):
             "note": "host wall time per call incl. two scalar read-backs (psnr)"}
 
 
+def hhffbpa_roofline(w, leaf_units, merge_units, newton_iterations, ms):
+    """SURVEY §8(d)'s path roofline: t_ideal = sum over stages of the time
+    the stage's work needs on its bounding unit at B200 peak, frac =
+    t_ideal / t_measured (never from BPA-equivalent work)."""
+    from paper_2506_23568_b200 import _native
+    peaks = measured_peaks()
+    sms = _native.library().hhsar_device_sm_count()
+    clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    hbm = float(peaks.get("hbm_gbs", 6542.1)) * 1e9
+    n_t = w.freqs.count * w.upsample
+    stages = {
+        # bytes: read the cube once, write the envelopes once
+        "range_compression": w.n_elements * (w.freqs.count + n_t) * 8 / hbm,
+        # ~150 FP64 instructions per iteration (10 sqrt/rsqrt + Jacobian +
+        # solve) at 64 lanes / clk / SM (measured 61, tools/bwk/pipes.cu)
+        "newton": newton_iterations * 150 / (64 * sms * clk),
+        # BPA unit: 3 MUFU at 16 / clk / SM
+        "leaf": leaf_units * 3 / (16 * sms * clk),
+        # merge unit (point x child): ~45 float64 instructions (4 corner
+        # distances, sqrt(r^2 - gap), n, phase) at 64 lanes / clk / SM
+        "merges_and_landing": merge_units * 45 / (64 * sms * clk),
+    }
+    t_ideal = sum(stages.values())
+    return {"t_ideal_ms": round(t_ideal * 1e3, 3), "frac": round(t_ideal * 1e3 / ms, 3),
+            "stages_ms": {k: round(v * 1e3, 3) for k, v in stages.items()},
+            "method": "SURVEY 8(d): sum over stages of work / bounding-unit peak (HBM "
+                      "MEASURED_PEAKS.json; MUFU 16, FP64 64 lanes/clk/SM at the max clock)"}
+
+
 def leaf_sweep_leg(dev, steps):
     """BASELINE config 2's sweep: HHFFBPA with merge factor 4 and leaves of
     8 / 16 / 32 frames (2^(M-1) balanced leaves of the 4,000 x 8 element
@@ -422,6 +451,7 @@ def hhffbpa_leg(index, dev, steps, check=False):
            "grids": int(sched.n_grids), "leaf_units": leaf_units, "merge_units": merge_units,
            "newton_iterations": int(stats[:, 4].sum()),
            "step": "range compression + grid plan/Newton + leaf BPA + merges + landing"}
+    out["roofline"] = hhffbpa_roofline(w, leaf_units, merge_units, int(stats[:, 4].sum()), ms)
     if check:
         import oracle
         from paper_2506_23568_b200.model import DataCube
