@@ -16,8 +16,11 @@
  *                             called via spectrum.invert_lattice, spectrum.py:327-407)
  *   hhsar_bpa_cartesian    <- bpa.bpa_reconstruct's meshgrid + backproject
  *                             (bpa.py:163-176)
- *   hhsar_range_demod      <- rangecomp.range_compress's pad + demodulation
- *                             (rangecomp.py:86-96; the IDFT itself is cuFFT)
+ *   hhsar_range_compress   <- rangecomp.range_compress (rangecomp.py:61-101):
+ *                             zero pad + IDFT + demodulation in one pass
+ *   hhsar_range_pad / hhsar_range_demod
+ *                          <- the same around a library IDFT (rangecomp.py:86-96),
+ *                             for n_t outside the fused kernel's sizes
  *   hhsar_volume_dot / hhsar_volume_residual <- metrics.psnr (metrics.py:126-150)
  *   hhsar_mip              <- metrics.max_intensity_projection (metrics.py:170-190)
  *   hhsar_leaf_boxes / hhsar_grid_plan / hhsar_grid_newton
@@ -29,8 +32,9 @@
  *                             (ffbp.py:336-340) fused with _downconvert_samples
  *                             (ffbp.py:343-348)
  *   hhsar_merge_level      <- ffbp.merge_pair / _merge_onto_points for every
- *                             parent of a level (ffbp.py:351-412), and the final
- *                             Cartesian landing (ffbp.py:493-495)
+ *                             parent of a level (ffbp.py:351-412)
+ *   hhsar_merge_cartesian  <- the final Cartesian landing (ffbp.py:493-495)
+ *   hhsar_downconvert      <- ffbp._downconvert_samples (ffbp.py:343-348)
  *   hhsar_simulate         <- simulator.simulate_measurement (simulator.py:41-69)
  */
 #ifndef HHSAR_B200_H
