@@ -163,6 +163,14 @@ int hhsar_range_demod(void *prof, int64_t n_el, int64_t n_t, double a, double dt
 int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t, double a,
                          double dt, void *out, void *stream);
 
+/* The same, keeping only delay bins [b0, b0 + w) of every row (a range
+ * gate): out[n_el][w], out[e][i] = envelope[e][b0 + i].  Bins outside the
+ * gate are neither stored nor, in the last radix-16 pass, computed.  An
+ * envelope gated this way is a profile with t0' = t0 + b0 dt and w bins. */
+int hhsar_range_compress_window(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
+                                double a, double dt, int64_t b0, int64_t w, void *out,
+                                void *stream);
+
 /* ---- HHFFBPA: grids ------------------------------------------------------ */
 
 /* 3-D bbox of every leaf's elements: el_pos float64 [N][3], bounds int64

@@ -55,6 +55,8 @@ SIGNATURES = {
     "hhsar_range_pad": ([_P, _I64, _I64, _I64, _P, _P], ctypes.c_int),
     "hhsar_range_demod": ([_P, _I64, _I64, _D, _D, _F, _P], ctypes.c_int),
     "hhsar_range_compress": ([_P, _I64, _I64, _I64, _D, _D, _P, _P], ctypes.c_int),
+    "hhsar_range_compress_window": ([_P, _I64, _I64, _I64, _D, _D, _I64, _I64, _P, _P],
+                                    ctypes.c_int),
     "hhsar_leaf_boxes": ([_P, _P, _I64, _P, _P], ctypes.c_int),
     "hhsar_grid_plan": ([_P, _I64, _P, _P, _I64, _P, _P, _P], ctypes.c_int),
     "hhsar_grid_newton": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),

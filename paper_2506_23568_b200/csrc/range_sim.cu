@@ -172,6 +172,15 @@ struct RcShape {
     static constexpr int THREADS = T * ROWS;
 };
 
+// e^{+2 pi i k / 16}, k < 16 (gated last pass)
+__constant__ float2 c_root16[16] = {
+    {1.f, 0.f}, {0.92387953f, 0.38268343f}, {0.70710678f, 0.70710678f},
+    {0.38268343f, 0.92387953f}, {0.f, 1.f}, {-0.38268343f, 0.92387953f},
+    {-0.70710678f, 0.70710678f}, {-0.92387953f, 0.38268343f}, {-1.f, 0.f},
+    {-0.92387953f, -0.38268343f}, {-0.70710678f, -0.70710678f}, {-0.38268343f, -0.92387953f},
+    {0.f, -1.f}, {0.38268343f, -0.92387953f}, {0.70710678f, -0.70710678f},
+    {0.92387953f, -0.38268343f}};
+
 // d[j + r T] = d[j] D^r (D = e^{j a dt T}): the demodulation of the last
 // pass needs one table entry per thread and these 16 constants (parameter
 // space, read as constant-bank operands).
@@ -183,7 +192,8 @@ template <int LOGN, int LOGUP>
 __global__ void __launch_bounds__(RcShape<LOGN>::THREADS, RcShape<LOGN>::THREADS >= 512 ? 2 : 4)
 range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
                       const float2 *__restrict__ tw, const float2 *__restrict__ demod,
-                      const __grid_constant__ RcDemodSteps steps, float2 *__restrict__ out) {
+                      const __grid_constant__ RcDemodSteps steps, float2 *__restrict__ out,
+                      int gate_b0, int gate_w) {
     using S = RcShape<LOGN>;
     constexpr int N = S::N, T = S::T;
     constexpr int R0 = S::REM > 0 ? (1 << S::REM) : 16;  // first-pass radix
@@ -198,7 +208,8 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
     const bool live = row < n_el;
     float2 *buf = rc_smem + ty * S::NP;
     const float2 *src = cube + (live ? row : 0) * n_f;
-    float2 *dst = out + row * N;
+    float2 *dst = out + row * gate_w - gate_b0;  // bin i lands at out[row][i - gate_b0]
+    const bool gated = gate_w < N;
 
     // outputs j + r T, r < 16, of the last pass: demodulate and store (coalesced)
     auto emit = [&](int j, float2 (&v)[16]) {
@@ -207,8 +218,10 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         if (live) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
+                const int i = j + r * T;
+                if (gated && (i < gate_b0 || i >= gate_b0 + gate_w)) continue;
                 const float2 u = cmul_p(v[r], as_x(steps.d[r]), as_x(steps.id[r]));
-                __stcs(dst + j + r * T, cmul_p(u, xdj, xidj));
+                __stcs(dst + i, cmul_p(u, xdj, xidj));
             }
         }
     };
@@ -235,6 +248,15 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
 #pragma unroll
     for (int p = (S::REM > 0 ? 0 : 1); p < P16; ++p) {
         const int j = tx, k = j & (ns - 1);
+        // gated output: this thread's outputs j + r T inside [gate_b0, gate_b0
+        // + gate_w) only; threads with none skip the last pass
+        int rlo = 0, rhi = 15;
+        if (gated && p == P16 - 1) {
+            rlo = max(0, (gate_b0 - j + T - 1) / T);
+            rhi = min(15, (gate_b0 + gate_w - 1 - j) / T);
+            if (gate_b0 + gate_w - 1 - j < 0) rhi = -1;
+            if (rlo > rhi) continue;  // last pass: nothing else follows
+        }
         float2 v[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = buf[rc_pad(j + r * T)];
@@ -251,6 +273,18 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         }
 #pragma unroll
         for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], w[r]);
+        if (gated && p == P16 - 1) {
+            // the few outputs this thread owns, each a direct 16-term sum
+            for (int r = rlo; r <= rhi; ++r) {
+                float2 y = v[0];
+#pragma unroll
+                for (int q = 1; q < 16; ++q) cfma(y, v[q], c_root16[(q * r) & 15]);
+                const int i = j + r * T;
+                if (live) __stcs(dst + i, cmul(y, __ldg(demod + i)));
+            }
+            ns *= 16;
+            continue;
+        }
         idft<16, 16>(v);
         if (p == P16 - 1) {
             emit(j, v);  // ns * 16 == N
@@ -267,7 +301,7 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
 
 template <int LOGN, int LOGUP>
 int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const float2 *demod,
-              const RcDemodSteps &steps, float2 *out, cudaStream_t s) {
+              const RcDemodSteps &steps, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
     using S = RcShape<LOGN>;
     const size_t smem = sizeof(float2) * S::NP * S::ROWS;
     auto kern = range_compress_kernel<LOGN, LOGUP>;
@@ -277,18 +311,19 @@ int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const
         const int64_t nb = groups - b0 < 2147483647ll ? groups - b0 : 2147483647ll;
         const int64_t r0 = b0 * S::ROWS;
         kern<<<(unsigned)nb, S::THREADS, smem, s>>>(cube + r0 * n_f, n_el - r0, n_f, tw, demod,
-                                                    steps, out + r0 * (int64_t)S::N);
+                                                    steps, out + r0 * (int64_t)gate_w, gate_b0,
+                                                    gate_w);
     }
     return check_launch("range_compress_kernel");
 }
 
 template <int LOGN>
 int launch_rc_up(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const float2 *demod,
-                 const RcDemodSteps &steps, float2 *out, cudaStream_t s) {
+                 const RcDemodSteps &steps, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
     const int64_t n = (int64_t)1 << LOGN;
-    if (n_f * 4 == n) return launch_rc<LOGN, 2>(cube, n_el, n_f, tw, demod, steps, out, s);
-    if (n_f * 8 == n) return launch_rc<LOGN, 3>(cube, n_el, n_f, tw, demod, steps, out, s);
-    return launch_rc<LOGN, 0>(cube, n_el, n_f, tw, demod, steps, out, s);
+    if (n_f * 4 == n) return launch_rc<LOGN, 2>(cube, n_el, n_f, tw, demod, steps, out, gate_b0, gate_w, s);
+    if (n_f * 8 == n) return launch_rc<LOGN, 3>(cube, n_el, n_f, tw, demod, steps, out, gate_b0, gate_w, s);
+    return launch_rc<LOGN, 0>(cube, n_el, n_f, tw, demod, steps, out, gate_b0, gate_w, s);
 }
 
 // One CTA per element; threads over frequencies.  Scatterer distances are
@@ -355,13 +390,15 @@ extern "C" int hhsar_range_demod(void *prof, int64_t n_el, int64_t n_t, double a
     return check_launch("range_demod_kernel");
 }
 
-extern "C" int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
-                                    double a, double dt, void *out, void *stream) {
+extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64_t n_f,
+                                           int64_t n_t, double a, double dt, int64_t b0,
+                                           int64_t w, void *out, void *stream) {
     HHSAR_REQUIRE(n_el >= 0 && n_f >= 1 && n_t >= n_f, "range_compress: bad sizes");
     int logn = 0;
     while ((1ll << logn) < n_t) ++logn;
     HHSAR_REQUIRE((1ll << logn) == n_t && logn >= 4 && logn <= 13,
                   "range_compress: n_t must be a power of two in [16, 8192]");
+    HHSAR_REQUIRE(b0 >= 0 && w >= 1 && b0 + w <= n_t, "range_compress: bad bin window");
     if (n_el == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
     float2 *tables = nullptr;  // twiddles [n_t], then demodulation phases [n_t]
@@ -381,20 +418,26 @@ extern "C" int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f,
         st.d[r] = make_float2((float)cos(red), (float)sin(red));
         st.id[r] = make_float2(-st.d[r].y, st.d[r].x);
     }
+    const int gb = (int)b0, gw = (int)w;
     switch (logn) {
-        case 4: rc = launch_rc_up<4>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 5: rc = launch_rc_up<5>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 6: rc = launch_rc_up<6>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 7: rc = launch_rc_up<7>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 8: rc = launch_rc_up<8>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 9: rc = launch_rc_up<9>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 10: rc = launch_rc_up<10>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 11: rc = launch_rc_up<11>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        case 12: rc = launch_rc_up<12>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
-        default: rc = launch_rc_up<13>(c, n_el, (int)n_f, tables, demod_tab, st, o, s); break;
+        case 4: rc = launch_rc_up<4>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 5: rc = launch_rc_up<5>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 6: rc = launch_rc_up<6>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 7: rc = launch_rc_up<7>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 8: rc = launch_rc_up<8>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 9: rc = launch_rc_up<9>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 10: rc = launch_rc_up<10>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 11: rc = launch_rc_up<11>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        case 12: rc = launch_rc_up<12>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
+        default: rc = launch_rc_up<13>(c, n_el, (int)n_f, tables, demod_tab, st, o, gb, gw, s); break;
     }
     cudaFreeAsync(tables, s);
     return rc;
+}
+
+extern "C" int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
+                                    double a, double dt, void *out, void *stream) {
+    return hhsar_range_compress_window(cube, n_el, n_f, n_t, a, dt, 0, n_t, out, stream);
 }
 
 extern "C" int hhsar_simulate(const double *el_pos, int64_t n_el, const double *pos,

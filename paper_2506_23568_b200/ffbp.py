@@ -448,34 +448,67 @@ def geometry_stream(device):
     return _GEO_STREAMS[key]
 
 
+def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
+    """Delay-bin window [b0, b0 + w) that holds every delay the leaf stage can
+    read.  A valid leaf point lies in its grid's slack box (ffbp.py:282-289,
+    containment) and a leaf element in the grid's element box, so every
+    point-element distance is within [min, max] of the box-to-box distances;
+    the leaf kernel's staging windows (triangle inequality around the box
+    centre) can overhang that by the element box's diagonal, plus 2 bins of
+    interpolation/rounding pad on each side.  Only the leaf stage reads
+    envelopes (merges read lattices), so profiles outside the gate are never
+    needed: config 4 keeps ~160 of 4,096 bins."""
+    d = lat.descs
+    a, b = sched.level_slices[0]
+    box = np.asarray(d["box"][a:b], dtype=np.float64)
+    blo, bhi = box[:, :3], box[:, 3:]
+    slo = np.asarray(d["slack_lo"][a:b], dtype=np.float64)
+    shi = np.asarray(d["slack_hi"][a:b], dtype=np.float64)
+    gap = np.maximum(0.0, np.maximum(blo - shi, slo - bhi))
+    far = np.maximum(np.abs(bhi - slo), np.abs(shi - blo))
+    d_min = float(np.sqrt((gap * gap).sum(axis=1)).min())
+    d_max = float(np.sqrt((far * far).sum(axis=1)).max())
+    diag = float(np.sqrt(((bhi - blo) ** 2).sum(axis=1)).max())
+    inv_bin = 2.0 / (C_LIGHT * dt)
+    margin = int(np.ceil(diag * inv_bin)) + 6
+    b0 = max(0, int(np.floor(d_min * inv_bin)) - margin)
+    b1 = min(n_t, int(np.ceil(d_max * inv_bin)) + margin + 1)
+    w = min(n_t - b0, -(-(b1 - b0) // 32) * 32)
+    return b0, w
+
+
 def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
                       levels: int, merge_factor: int = 2, upsample: int = 8,
-                      vox_range=None) -> DeviceRun:
-    """Whole HHFFBPA step from a device cube with the grid construction
-    overlapped with range compression: the lattices depend only on geometry,
-    so plan + Newton run on a side stream while the main stream
-    range-compresses; the leaf stage waits for both."""
+                      vox_range=None, gate: bool = True) -> DeviceRun:
+    """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
+    high-priority side stream; once the plan's descriptors are on the host
+    the range compression is launched on the caller's stream for the delay
+    bins the leaf stage can read only (leaf_range_gate; ``gate=False``
+    computes full profiles); the leaf stage waits for both."""
     import torch
-    from .rangecomp import profile_axis, range_compress_device
+    from .rangecomp import profile_axis, range_compress_device, range_compress_window
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
     window_hi = 0.0 + (n_t - 1) * dt
     main = torch.cuda.current_stream()
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
-    # the (cached) plan set-up is launched first on the high-priority stream,
-    # then the range compression; the host waits only for the plan
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)
-    env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
+    if not gate:
+        env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
+        t0 = 0.0
     with torch.cuda.stream(geo):
         lat = finish_lattices(pending)
+    if gate:
+        b0, w = leaf_range_gate(lat, sched, dt, n_t)
+        env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
     main.wait_stream(geo)
     # blocks allocated on the side stream are used on the main one from here
     for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
         t.record_stream(main)
-    pipe = Pipeline(env, el_dev, el4, 0.0, dt, k_ref, kgrid, region, final_dims, params, levels,
+    pipe = Pipeline(env, el_dev, el4, t0, dt, k_ref, kgrid, region, final_dims, params, levels,
                     merge_factor, window_hi, sched=sched, lat=lat)
     return pipe.run(vox_range)
 

@@ -108,6 +108,23 @@ def range_compress_device(cube_dev, freqs, upsample: int = 8):
     return prof, dt, k_ref
 
 
+def range_compress_window(cube_dev, freqs, upsample: int, b0: int, w: int):
+    """Device cube -> the delay-bin window [b0, b0 + w) of every envelope row
+    (hhsar_range_compress_window).  Returns (envelopes [N_el, w], t0', dt,
+    k_ref): the gated rows are profiles starting at t0' = b0 dt."""
+    import torch
+    n_t, dt, k_ref, a = profile_axis(freqs, upsample)
+    if not (16 <= n_t <= 8192 and n_t & (n_t - 1) == 0):
+        env, dt, k_ref = range_compress_device(cube_dev, freqs, upsample)
+        return env[:, b0:b0 + w].contiguous(), b0 * dt, dt, k_ref
+    cube_dev = cube_dev.to(torch.complex64).contiguous()
+    prof = torch.empty((cube_dev.shape[0], w), dtype=torch.complex64, device=cube_dev.device)
+    _native.call("hhsar_range_compress_window", _native.ptr(cube_dev), cube_dev.shape[0],
+                 cube_dev.shape[1], n_t, a, dt, int(b0), int(w), _native.ptr(prof),
+                 _native.stream_handle())
+    return prof, b0 * dt, dt, k_ref
+
+
 def range_compress(cube, upsample: int = 8, device="cuda") -> RangeProfileSet:
     """range_compress (rangecomp.py:61-101) on the GPU."""
     import torch

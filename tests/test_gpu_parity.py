@@ -322,3 +322,49 @@ def test_config3_full_scale_vs_oracle(hh):
           for k, (a, b) in enumerate(run.sched.level_slices)]
     assert lp == prov["level_points"][:-1]
     assert [int(f) for f in run.flags.cpu().numpy()] == prov["merge_flags"] + [prov["final_flags"]]
+
+
+@pytest.mark.parametrize("n_el,n_f,upsample,b0,w", [(37, 256, 4, 80, 96), (9, 512, 4, 0, 64),
+                                                    (5, 1024, 4, 4000, 96), (3, 128, 8, 300, 211),
+                                                    (4, 64, 4, 17, 239)])
+def test_range_compress_window_equals_full_slice(n_el, n_f, upsample, b0, w):
+    """The range-gated compression (only bins [b0, b0 + w) computed in the
+    last pass and stored) against the same bins of the full compression."""
+    import torch
+    from paper_2506_23568_b200 import rangecomp
+    from paper_2506_23568_b200.model import FrequencyGrid
+    freqs = FrequencyGrid(77e9, 81e9, n_f)
+    gen = torch.Generator(device="cuda").manual_seed(n_el * 31 + n_f)
+    cube = torch.randn((n_el, n_f), dtype=torch.complex64, device="cuda", generator=gen)
+    full, dt, k_ref = rangecomp.range_compress_device(cube, freqs, upsample)
+    got, t0w, dt2, k2 = rangecomp.range_compress_window(cube, freqs, upsample, b0, w)
+    assert (dt2, k2) == (dt, k_ref) and t0w == b0 * dt and got.shape == (n_el, w)
+    want = full[:, b0:b0 + w]
+    assert rel_l2(got.cpu().numpy(), want.cpu().numpy()) < 2e-6
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_range_gate_matches_full_profiles(config):
+    """HHFFBPA with range-gated compression (only the delay bins the leaf
+    stage can read, ffbp.leaf_range_gate) equals the run on full profiles:
+    same image to float rounding, same lattices and flags, no leaf delay
+    outside the gated window."""
+    import torch
+    from paper_2506_23568_b200 import bpa, ffbp, workloads
+    w = workloads.config(config)
+    gen = torch.Generator(device="cuda").manual_seed(w.seed)
+    cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
+                       generator=gen)
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    el4 = bpa.el_f32x4(el)
+    params = ffbp.FfbpParams(levels=w.levels)
+    runs = [ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params, w.levels,
+                                   w.merge_factor, w.upsample, gate=g) for g in (False, True)]
+    torch.cuda.synchronize()
+    full, gated = (r.volume.cpu().numpy() for r in runs)
+    assert int(runs[1].oow.cpu()[0]) == int(runs[0].oow.cpu()[0]) == 0
+    rel = np.linalg.norm(gated - full) / np.linalg.norm(full)
+    assert rel < 1e-5, rel
+    assert np.argmax(np.abs(gated)) == np.argmax(np.abs(full))
+    assert torch.equal(runs[0].lattices.stats, runs[1].lattices.stats)
+    assert torch.equal(runs[0].flags, runs[1].flags)
