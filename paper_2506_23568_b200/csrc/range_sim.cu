@@ -260,6 +260,29 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         float2 v[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = buf[rc_pad(j + r * T)];
+        if (gated && p == P16 - 1) {
+            // the few outputs i = j + r T this thread owns: y = sum_q v[q] z^q
+            // with z = e^{2 pi i i / N} = w (e^{2 pi i / 16})^r, evaluated as
+            // two 8-term Horner chains A + z^8 B (z^8 = +-w^8) -- no twiddle
+            // products for the 15 inputs, 2 FFMA2 per term
+            const float2 w1 = __ldg(tw + twoff + k), w8 = __ldg(tw + twoff + 3 * ns + k);
+            for (int r = rlo; r <= rhi; ++r) {
+                const float2 z = cmul(w1, c_root16[r]);
+                const f2x xz = as_x(z), xiz = pk2(-z.y, z.x);
+                f2x a = as_x(v[7]), b = as_x(v[15]);
+#pragma unroll
+                for (int q = 6; q >= 0; --q) {
+                    a = fma2(bc2(hi2(a)), xiz, fma2(bc2(lo2(a)), xz, as_x(v[q])));
+                    b = fma2(bc2(hi2(b)), xiz, fma2(bc2(lo2(b)), xz, as_x(v[q + 8])));
+                }
+                const float2 z8 = (r & 1) ? make_float2(-w8.x, -w8.y) : w8;
+                const float2 y = as_f(fma2(bc2(hi2(b)), pk2(-z8.y, z8.x),
+                                           fma2(bc2(lo2(b)), as_x(z8), a)));
+                const int i = j + r * T;
+                if (live) __stcs(dst + i, cmul(y, __ldg(demod + i)));
+            }
+            continue;  // last pass
+        }
         // w^1, w^2, w^4, w^8 by four coalesced loads, the other powers by
         // products (<= 3 roundings)
         float2 w[16];
@@ -273,18 +296,6 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         }
 #pragma unroll
         for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], w[r]);
-        if (gated && p == P16 - 1) {
-            // the few outputs this thread owns, each a direct 16-term sum
-            for (int r = rlo; r <= rhi; ++r) {
-                float2 y = v[0];
-#pragma unroll
-                for (int q = 1; q < 16; ++q) cfma(y, v[q], c_root16[(q * r) & 15]);
-                const int i = j + r * T;
-                if (live) __stcs(dst + i, cmul(y, __ldg(demod + i)));
-            }
-            ns *= 16;
-            continue;
-        }
         idft<16, 16>(v);
         if (p == P16 - 1) {
             emit(j, v);  // ns * 16 == N

@@ -448,6 +448,9 @@ def geometry_stream(device):
     return _GEO_STREAMS[key]
 
 
+GATE_MIN_BYTES = 8 << 30
+
+
 def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
     """Delay-bin window [b0, b0 + w) that holds every delay the leaf stage can
     read.  A valid leaf point lies in its grid's slack box (ffbp.py:282-289,
@@ -479,12 +482,16 @@ def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
 
 def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
                       levels: int, merge_factor: int = 2, upsample: int = 8,
-                      vox_range=None, gate: bool = True) -> DeviceRun:
+                      vox_range=None, gate=None) -> DeviceRun:
     """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
     high-priority side stream; once the plan's descriptors are on the host
     the range compression is launched on the caller's stream for the delay
     bins the leaf stage can read only (leaf_range_gate; ``gate=False``
-    computes full profiles); the leaf stage waits for both."""
+    computes full profiles); the leaf stage waits for both.  The gate costs
+    the plan's host round trip ahead of the compression, so by default
+    (``gate=None``) it is used when full profiles would exceed
+    GATE_MIN_BYTES (config 4: 68.7 GB of profiles -> 4.8 GB, 18.9 -> 16.8 ms;
+    config 3 loses ~0.2 ms to the wait and stays ungated)."""
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
@@ -493,6 +500,8 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
+    if gate is None:
+        gate = int(cube_dev.shape[0]) * n_t * 8 > GATE_MIN_BYTES
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)
