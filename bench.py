@@ -322,7 +322,7 @@ def metrics_leg(volume, dims):
             "note": "host wall time per call incl. two scalar read-backs (psnr)"}
 
 
-def hhffbpa_roofline(w, leaf_units, merge_units, newton_iterations, ms):
+def hhffbpa_roofline(w, leaf_units, merge_units, newton_iterations, ms, bins_written=None):
     """SURVEY §8(d)'s path roofline: t_ideal = sum over stages of the time
     the stage's work needs on its bounding unit at B200 peak, frac =
     t_ideal / t_measured (never from BPA-equivalent work)."""
@@ -333,8 +333,9 @@ def hhffbpa_roofline(w, leaf_units, merge_units, newton_iterations, ms):
     hbm = float(peaks.get("hbm_gbs", 6542.1)) * 1e9
     n_t = w.freqs.count * w.upsample
     stages = {
-        # bytes: read the cube once, write the envelopes once
-        "range_compression": w.n_elements * (w.freqs.count + n_t) * 8 / hbm,
+        # bytes: read the cube once, write the envelopes once (only the
+        # range-gated bins when the step gates, ffbp.leaf_range_gate)
+        "range_compression": w.n_elements * (w.freqs.count + (bins_written or n_t)) * 8 / hbm,
         # ~150 FP64 instructions per iteration (10 sqrt/rsqrt + Jacobian +
         # solve) at 64 lanes / clk / SM (measured 61, tools/bwk/pipes.cu)
         "newton": newton_iterations * 150 / (64 * sms * clk),
@@ -451,7 +452,12 @@ def hhffbpa_leg(index, dev, steps, check=False):
            "grids": int(sched.n_grids), "leaf_units": leaf_units, "merge_units": merge_units,
            "newton_iterations": int(stats[:, 4].sum()),
            "step": "range compression + grid plan/Newton + leaf BPA + merges + landing"}
-    out["roofline"] = hhffbpa_roofline(w, leaf_units, merge_units, int(stats[:, 4].sum()), ms)
+    n_t, dt, _, _ = rangecomp.profile_axis(w.freqs, w.upsample)
+    gate = ffbp.leaf_range_gate(run.lattices, sched, dt, n_t)
+    bins = gate[1]
+    out["range_gate"] = {"b0": gate[0], "bins": gate[1], "of": n_t}
+    out["roofline"] = hhffbpa_roofline(w, leaf_units, merge_units, int(stats[:, 4].sum()), ms,
+                                       bins)
     if check:
         import oracle
         from paper_2506_23568_b200.model import DataCube

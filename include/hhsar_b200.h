@@ -72,8 +72,8 @@ typedef struct hhsar_geom {
 } hhsar_geom;
 
 /* One subimage lattice.  Filled by hhsar_grid_plan (bounds, dims, masks'
- * index ranges) except start/stop/leaf range (host) and offset/col_offset
- * (host prefix sums once dims are known). */
+ * index ranges, and offset/col_offset when it is given `totals`) except
+ * start/stop/leaf range (host). */
 typedef struct hhsar_grid_desc {
     double ext[4];       /* lateral element bbox x_min,x_max,y_min,y_max       */
     double box[6];       /* 3-D element bbox: lo xyz, hi xyz                   */
@@ -183,10 +183,14 @@ int hhsar_leaf_boxes(const double *el_pos, const int64_t *bounds, int64_t n_leav
  * (int32, device) receives 1 if any boundary point is outside the
  * compressed-coordinate domain (spectrum.py:253-255).  grids, leaf_box,
  * boundary, status are device pointers; geom is a HOST pointer (as in every
- * call taking an hhsar_geom). */
+ * call taking an hhsar_geom).  totals (int64 [2], device, optional): when
+ * given, every desc.offset / desc.col_offset is set to the exclusive prefix
+ * sum of the lattice sizes / active-column counts in grid order and
+ * totals = {lattice points, active columns} (the pool and work-list sizes
+ * hhsar_grid_newton needs), so the host reads them back with the descs. */
 int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_box,
                     const double *boundary, int64_t n_b, const hhsar_geom *geom,
-                    int32_t *status, void *stream);
+                    int32_t *status, int64_t *totals, void *stream);
 
 /* Newton inversion of every ACTIVE (u, v) column of every grid (desc.act_*
  * rectangle, at desc.col_offset in a work list of n_cols columns), warm

@@ -58,7 +58,7 @@ SIGNATURES = {
     "hhsar_range_compress_window": ([_P, _I64, _I64, _I64, _D, _D, _I64, _I64, _P, _P],
                                     ctypes.c_int),
     "hhsar_leaf_boxes": ([_P, _P, _I64, _P, _P], ctypes.c_int),
-    "hhsar_grid_plan": ([_P, _I64, _P, _P, _I64, _P, _P, _P], ctypes.c_int),
+    "hhsar_grid_plan": ([_P, _I64, _P, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
     "hhsar_grid_newton": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "hhsar_volume_dot": ([_P, _P, _I64, _I32, _P, _P], ctypes.c_int),
     "hhsar_volume_residual": ([_P, _P, _I64, _I32, _D, _D, _P, _P], ctypes.c_int),
@@ -115,20 +115,28 @@ def exported_symbols() -> list[str]:
     return list(SIGNATURES)
 
 
+_fns = {}
+
+
 def call(name: str, *args) -> None:
     """Invoke an entry point; raise RuntimeError with the library's message
     on a non-zero status (argument errors are pre-validated by callers)."""
-    lib = library()
-    status = getattr(lib, name)(*args)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(library(), name)
+    status = fn(*args)
     if status != 0:
-        msg = lib.hhsar_last_error().decode(errors="replace")
+        msg = library().hhsar_last_error().decode(errors="replace")
         raise RuntimeError(f"{name} failed (status {status}): {msg}")
 
 
 def stream_handle(stream=None):
+    """cudaStream_t of `stream` (default: torch's current stream on the
+    current device, read without constructing a Stream object)."""
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def ptr(t) -> ctypes.c_void_p:

@@ -655,14 +655,91 @@ extern "C" int hhsar_leaf_boxes(const double *el_pos, const int64_t *bounds, int
     return check_launch("leaf_boxes_kernel");
 }
 
+// offset / col_offset of every grid as exclusive prefix sums of the lattice
+// sizes and active-column counts the plan just wrote, totals[0] = points,
+// totals[1] = columns (one CTA: a few thousand grids at most).
+constexpr int SCAN_THREADS = 1024;
+__global__ void __launch_bounds__(SCAN_THREADS)
+grid_offsets_kernel(hhsar_grid_desc *__restrict__ grids, int n, int64_t *__restrict__ totals) {
+    __shared__ int64_t s_p[SCAN_THREADS / 32], s_c[SCAN_THREADS / 32];
+    const int per = (n + SCAN_THREADS - 1) / SCAN_THREADS;
+    const int a = min(n, (int)threadIdx.x * per), b = min(n, a + per);
+    auto sizes = [&](int i, int64_t &pts, int64_t &cols) {
+        const hhsar_grid_desc &D = grids[i];
+        pts = (int64_t)D.dims[0] * D.dims[1] * D.dims[2];
+        const int64_t su = max(D.act_hi[0] - D.act_lo[0] + 1, 0);
+        const int64_t sv = max(D.act_hi[1] - D.act_lo[1] + 1, 0);
+        cols = su * sv;
+    };
+    int64_t p = 0, c = 0;
+    for (int i = a; i < b; ++i) {
+        int64_t pi, ci;
+        sizes(i, pi, ci);
+        p += pi;
+        c += ci;
+    }
+    // block-wide exclusive scan of (p, c)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t ip = p, ic = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t tp = __shfl_up_sync(0xffffffffu, ip, o);
+        const int64_t tc = __shfl_up_sync(0xffffffffu, ic, o);
+        if (lane >= o) {
+            ip += tp;
+            ic += tc;
+        }
+    }
+    if (lane == 31) {
+        s_p[wid] = ip;
+        s_c[wid] = ic;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        int64_t wp = s_p[lane], wc = s_c[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t tp = __shfl_up_sync(0xffffffffu, wp, o);
+            const int64_t tc = __shfl_up_sync(0xffffffffu, wc, o);
+            if (lane >= o) {
+                wp += tp;
+                wc += tc;
+            }
+        }
+        s_p[lane] = wp;
+        s_c[lane] = wc;
+    }
+    __syncthreads();
+    int64_t op = ip - p + (wid ? s_p[wid - 1] : 0), oc = ic - c + (wid ? s_c[wid - 1] : 0);
+    for (int i = a; i < b; ++i) {
+        int64_t pi, ci;
+        sizes(i, pi, ci);
+        grids[i].offset = op;
+        grids[i].col_offset = oc;
+        op += pi;
+        oc += ci;
+    }
+    if (threadIdx.x == SCAN_THREADS - 1) {
+        totals[0] = op;
+        totals[1] = oc;
+    }
+}
+
 extern "C" int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_box,
                                const double *boundary, int64_t n_b, const hhsar_geom *geom,
-                               int32_t *status, void *stream) {
+                               int32_t *status, int64_t *totals, void *stream) {
     HHSAR_REQUIRE(n_grids > 0 && n_grids < (1ll << 31), "grid_plan: bad grid count");
     HHSAR_REQUIRE(n_b > 0 && geom != nullptr, "grid_plan: bad boundary lattice");
     HHSAR_REQUIRE(geom->step > 0.0 && geom->step <= 1.0, "grid_plan: step must lie in (0, 1]");
     grid_plan_kernel<<<(unsigned)n_grids, PLAN_THREADS, 0, as_stream(stream)>>>(
         grids, leaf_box, boundary, (int)n_b, *geom, status);
+    if (totals != nullptr) {
+        int rc = check_launch("grid_plan_kernel");
+        if (rc) return rc;
+        grid_offsets_kernel<<<1, SCAN_THREADS, 0, as_stream(stream)>>>(grids, (int)n_grids,
+                                                                        totals);
+        return check_launch("grid_offsets_kernel");
+    }
     return check_launch("grid_plan_kernel");
 }
 

@@ -138,20 +138,34 @@ class Schedule:
 def make_geom(region, kgrid, gamma: float, margin: float, pad: int, window_hi: float,
               tol: float = 1e-9, max_iter: int = 50, z_floor: float = 1e-4) -> np.ndarray:
     """hhsar_geom with every constant computed in float64 exactly as the
-    reference computes it (spectrum.py:256-272, ffbp.py:241-269)."""
+    reference computes it (spectrum.py:256-272, ffbp.py:241-269).  Cached
+    per argument set (read-only: native calls only read it)."""
     k_min, k_max = kgrid.k_min, kgrid.k_max
+    key = (_region_tuple(region), float(k_min), float(k_max), float(gamma), float(margin),
+           int(pad), float(window_hi), float(tol), int(max_iter), float(z_floor))
+    hit = _GEOMS.get(key)
+    if hit is not None:
+        return hit
     extents = (region.x_max - region.x_min, region.y_max - region.y_min,
                region.z_max - region.z_min)
     diag = float(getattr(region, "diagonal", np.linalg.norm(extents)))
     center = [(region.x_min + region.x_max) / 2, (region.y_min + region.y_max) / 2,
               (region.z_min + region.z_max) / 2]
-    return _native.host_struct(_native.GEOM_DTYPE, dict(
+    geom = _native.host_struct(_native.GEOM_DTYPE, dict(
         region=[region.x_min, region.x_max, region.y_min, region.y_max, region.z_min,
                 region.z_max],
         center=center, k_min=k_min, k_max=k_max, c_uv=k_max / np.pi,
         c_nhi=k_max / (2.0 * TWO_PI), c_nlo=k_min / (2.0 * TWO_PI),
         step=np.full(3, 1.0 / gamma)[0], margin=margin, max_step=0.5 * diag, tol=tol,
         z_floor=z_floor, window_hi=window_hi, pad=pad, max_iter=max_iter))
+    geom.setflags(write=False)
+    if len(_GEOMS) > 64:
+        _GEOMS.clear()
+    _GEOMS[key] = geom
+    return geom
+
+
+_GEOMS = {}
 
 
 # ---------------------------------------------------------------------------
@@ -215,7 +229,7 @@ def _plan_upload(sched: Schedule, region):
         return hit[:3]
     bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
     parts = [sched.grids.view(np.uint8).reshape(-1), sched.bounds.astype(np.int64).view(np.uint8),
-             bl.view(np.uint8).reshape(-1), np.zeros(8, dtype=np.uint8)]
+             bl.view(np.uint8).reshape(-1), np.zeros(24, dtype=np.uint8)]
     cuts = np.cumsum([0] + [p.size for p in parts])
     staged = torch.empty(int(cuts[-1]), dtype=torch.uint8, pin_memory=True)
     sn = staged.numpy()
@@ -245,20 +259,23 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     descs_dev = up[cuts[0]:cuts[1]]
     bounds = up[cuts[1]:cuts[2]]
     boundary = up[cuts[2]:cuts[3]]
-    status = up[cuts[3]:cuts[4]]
+    status = up[cuts[3]:cuts[4]]  # int32 status, pad, int64 totals[2]
     leaf_box = torch.empty((sched.n_leaves, 6), dtype=torch.float64, device=dev)
     _native.call("hhsar_leaf_boxes", _native.ptr(el_dev), _native.ptr(bounds), sched.n_leaves,
                  _native.ptr(leaf_box), stream)
     geom = make_geom(region, kgrid, gamma, margin, pad, window_hi, tol, max_iter)
+    # the plan also writes every grid's pool offset / work-list offset and
+    # the two totals, so the host only reads them back
     _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
-                 _native.ptr(boundary), n_b, _native.ptr(geom), _native.ptr(status), stream)
-    back = torch.empty(int(cuts[1]) + 8, dtype=torch.uint8, pin_memory=True)
+                 _native.ptr(boundary), n_b, _native.ptr(geom), _native.ptr(status),
+                 _native.c_void_p_offset(status, 8), stream)
+    back = torch.empty(int(cuts[1]) + 24, dtype=torch.uint8, pin_memory=True)
     back[:cuts[1]].copy_(descs_dev, non_blocking=True)
     back[cuts[1]:].copy_(status, non_blocking=True)
     done = torch.cuda.Event()
     done.record()
     return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
-                host_d=back[:cuts[1]], host_s=back[cuts[1]:cuts[1] + 4].view(torch.int32),
+                host_d=back[:cuts[1]], host_s=back[cuts[1]:].numpy(),
                 done=done, back=back, keep=(staged, up, leaf_box))
 
 
@@ -277,35 +294,25 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     # the plan's pinned read-back IS the host descriptor table from here on
     # (edited in place, uploaded from, kept alive with the lattices)
     host = p["host_d"].numpy().view(_native.GRID_DTYPE)
-    if int(p["host_s"][0]):
+    status = p["host_s"]
+    if int(status[:4].view(np.int32)[0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
-    dims = host["dims"].astype(np.int64)
-    npts = dims[:, 0] * dims[:, 1] * dims[:, 2]
-    offsets = np.cumsum(npts)
-    total = int(offsets[-1])
-    host["offset"][0] = 0
-    host["offset"][1:] = offsets[:-1]
-    # Newton work list: the active (u, v) rectangle of every grid (the kernel
-    # finds a column's grid by binary search over col_offset)
-    span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
-    cols = span[:, 0] * span[:, 1]
+    # offsets, column offsets and both totals came from the plan (device scan)
+    total, n_cols = (int(v) for v in status[8:24].view(np.int64))
     if newton_grids is not None:
-        cols = np.where(np.asarray(newton_grids, dtype=bool), cols, 0)
-    starts = np.cumsum(cols)
-    n_cols = int(starts[-1])
-    host["col_offset"][0] = 0
-    host["col_offset"][1:] = starts[:-1]
+        # Newton work list restricted to the selected grids: re-derive the
+        # column offsets and send the descriptors back up
+        span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
+        cols = np.where(np.asarray(newton_grids, dtype=bool), span[:, 0] * span[:, 1], 0)
+        starts = np.cumsum(cols)
+        n_cols = int(starts[-1])
+        host["col_offset"][0] = 0
+        host["col_offset"][1:] = starts[:-1]
+        back, up = p["back"], p["keep"][1]
+        nb = host.nbytes
+        up[:nb].copy_(back[:nb], non_blocking=True)
     if _trace:
         _trace("worklist built")
-    # descriptors go back up through the plan's pinned read-back buffer (its
-    # D2H copy completed: we synchronised on it) into the plan's device copy
-    back, up = p["back"], p["keep"][1]
-    nb = host.nbytes
-    up[:nb].copy_(back[:nb], non_blocking=True)
-    staged = back
-    descs_dev = up[:nb]
-    if _trace:
-        _trace("descs uploaded")
     positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
     valid = torch.zeros(total, dtype=torch.uint8, device=dev)
     stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
@@ -315,7 +322,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
                  None, _native.ptr(geom), _native.ptr(positions), _native.ptr(valid),
                  _native.ptr(stats), stream)
     lat = Lattices(host, descs_dev, positions, valid, stats, geom)
-    lat.keep = (staged, up)  # pinned staging must outlive the async copy
+    lat.keep = (p["back"], p["keep"][1])  # pinned staging must outlive the async copy
     return lat
 
 
@@ -448,9 +455,6 @@ def geometry_stream(device):
     return _GEO_STREAMS[key]
 
 
-GATE_MIN_BYTES = 8 << 30
-
-
 def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
     """Delay-bin window [b0, b0 + w) that holds every delay the leaf stage can
     read.  A valid leaf point lies in its grid's slack box (ffbp.py:282-289,
@@ -482,16 +486,17 @@ def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
 
 def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
                       levels: int, merge_factor: int = 2, upsample: int = 8,
-                      vox_range=None, gate=None) -> DeviceRun:
+                      vox_range=None, gate: bool = True) -> DeviceRun:
     """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
     high-priority side stream; once the plan's descriptors are on the host
     the range compression is launched on the caller's stream for the delay
     bins the leaf stage can read only (leaf_range_gate; ``gate=False``
-    computes full profiles); the leaf stage waits for both.  The gate costs
-    the plan's host round trip ahead of the compression, so by default
-    (``gate=None``) it is used when full profiles would exceed
-    GATE_MIN_BYTES (config 4: 68.7 GB of profiles -> 4.8 GB, 18.9 -> 16.8 ms;
-    config 3 loses ~0.2 ms to the wait and stays ungated)."""
+    computes full profiles); the leaf stage waits for both.  The gate puts
+    the plan's host round trip ahead of the compression but shrinks the
+    profiles to the leaf stage's reach (config 2/3/4: 256/352/288 of
+    1,024/2,048/4,096 bins; config 4 68.7 GB of profiles -> 4.8 GB, RC
+    18.9 -> 14.6 ms; config 3 2.67 -> 2.57 ms per step).
+    """
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
@@ -500,8 +505,6 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
-    if gate is None:
-        gate = int(cube_dev.shape[0]) * n_t * 8 > GATE_MIN_BYTES
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi)
@@ -609,8 +612,15 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
     if region.z_min <= 0.0:
         raise ConfigError("region must sit strictly in front of the array")
     partition_subarrays(cube.aperture, levels)  # raises ConfigError when too deep
-    run = hhffbpa_from_cube(to_device_cube(cube.values), el_dev, el_f32x4(el_dev), kgrid,
-                            region, final_dims, params, levels, merge_factor, upsample)
+    cube_dev = to_device_cube(cube.values)
+    run = hhffbpa_from_cube(cube_dev, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
+                            params, levels, merge_factor, upsample)
+    if int(run.oow.cpu()[0]):
+        # a leaf delay outside the range gate (the gate is a geometric bound;
+        # this never fired on the BASELINE configs): redo on full profiles so
+        # the out-of-window verdict is the reference's
+        run = hhffbpa_from_cube(cube_dev, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
+                                params, levels, merge_factor, upsample, gate=False)
     extra = torch.cat([run.flags, run.lattices.stats.reshape(-1)])
     volume, tail = _finish(run.volume, run.oow, final_dims, origin, step, {}, extra)
     n_flags = run.flags.numel()
