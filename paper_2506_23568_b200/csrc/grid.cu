@@ -725,6 +725,76 @@ grid_offsets_kernel(hhsar_grid_desc *__restrict__ grids, int n, int64_t *__restr
     }
 }
 
+// Delay-bin window [b0, b0 + w) the leaf stage can read (ffbp.leaf_range_gate
+// restated; same float64 operations, so the same integers): valid leaf points
+// lie in their grid's slack box and leaf elements in its element box, so
+// every leaf delay lies between the boxes' nearest and farthest distances;
+// the margin covers the leaf kernel's staging overhang (element-box
+// diagonal) plus interpolation / rounding pad.  One CTA.
+__global__ void __launch_bounds__(SCAN_THREADS)
+leaf_gate_kernel(const hhsar_grid_desc *__restrict__ leaves, int n, double inv_bin, int64_t n_t,
+                 int64_t *__restrict__ gate) {
+    __shared__ double s_lo[SCAN_THREADS / 32], s_hi[SCAN_THREADS / 32], s_dg[SCAN_THREADS / 32];
+    double dmin = DBL_MAX, dmax = 0.0, diag = 0.0;
+    for (int i = threadIdx.x; i < n; i += SCAN_THREADS) {
+        const hhsar_grid_desc &D = leaves[i];
+        double g2 = 0.0, f2 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double blo = D.box[a], bhi = D.box[3 + a], slo = D.slack_lo[a],
+                         shi = D.slack_hi[a];
+            const double gap = fmax(0.0, fmax(blo - shi, slo - bhi));
+            const double far = fmax(fabs(bhi - slo), fabs(shi - blo));
+            const double ext = bhi - blo;
+            // no FMA contraction: the same roundings as the numpy form
+            g2 = a ? __dadd_rn(g2, __dmul_rn(gap, gap)) : __dmul_rn(gap, gap);
+            f2 = a ? __dadd_rn(f2, __dmul_rn(far, far)) : __dmul_rn(far, far);
+            d2 = a ? __dadd_rn(d2, __dmul_rn(ext, ext)) : __dmul_rn(ext, ext);
+        }
+        dmin = fmin(dmin, sqrt(g2));
+        dmax = fmax(dmax, sqrt(f2));
+        diag = fmax(diag, sqrt(d2));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        diag = fmax(diag, __shfl_xor_sync(0xffffffffu, diag, o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_lo[wid] = dmin;
+        s_hi[wid] = dmax;
+        s_dg[wid] = diag;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < SCAN_THREADS / 32; ++k) {
+            dmin = fmin(dmin, s_lo[k]);
+            dmax = fmax(dmax, s_hi[k]);
+            diag = fmax(diag, s_dg[k]);
+        }
+        const int64_t margin = (int64_t)ceil(__dmul_rn(diag, inv_bin)) + 6;
+        int64_t b0 = (int64_t)floor(__dmul_rn(dmin, inv_bin)) - margin;
+        b0 = b0 > 0 ? b0 : 0;
+        int64_t b1 = (int64_t)ceil(__dmul_rn(dmax, inv_bin)) + margin + 1;
+        b1 = b1 < n_t ? b1 : n_t;
+        int64_t w = (b1 - b0 + 31) / 32 * 32;
+        w = w < n_t - b0 ? w : n_t - b0;
+        gate[0] = b0;
+        gate[1] = w;
+    }
+}
+
+extern "C" int hhsar_leaf_range_gate(const hhsar_grid_desc *leaves, int64_t n_leaves, double dt,
+                                     int64_t n_t, int64_t *gate, void *stream) {
+    HHSAR_REQUIRE(n_leaves > 0 && n_leaves < (1ll << 31) && dt > 0.0 && n_t > 0,
+                  "leaf_range_gate: bad arguments");
+    leaf_gate_kernel<<<1, SCAN_THREADS, 0, as_stream(stream)>>>(
+        leaves, (int)n_leaves, 2.0 / (HHSAR_C_LIGHT * dt), n_t, gate);
+    return check_launch("leaf_gate_kernel");
+}
+
 extern "C" int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_box,
                                const double *boundary, int64_t n_b, const hhsar_geom *geom,
                                int32_t *status, int64_t *totals, void *stream) {

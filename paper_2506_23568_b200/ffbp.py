@@ -189,6 +189,7 @@ class Lattices:
         self.geom = geom
         self.npts = np.prod(descs["dims"].astype(np.int64), axis=1)
         self.values = None
+        self.gate = None
 
     def desc_ptr(self, g: int):
         import ctypes
@@ -229,7 +230,7 @@ def _plan_upload(sched: Schedule, region):
         return hit[:3]
     bl = np.ascontiguousarray(boundary_lattice(region, BOUNDARY_PER_AXIS))
     parts = [sched.grids.view(np.uint8).reshape(-1), sched.bounds.astype(np.int64).view(np.uint8),
-             bl.view(np.uint8).reshape(-1), np.zeros(24, dtype=np.uint8)]
+             bl.view(np.uint8).reshape(-1), np.zeros(40, dtype=np.uint8)]
     cuts = np.cumsum([0] + [p.size for p in parts])
     staged = torch.empty(int(cuts[-1]), dtype=torch.uint8, pin_memory=True)
     sn = staged.numpy()
@@ -246,20 +247,26 @@ def _region_tuple(region):
 
 
 def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float, pad: int,
-                  window_hi: float, tol: float = 1e-9, max_iter: int = 50):
+                  window_hi: float, tol: float = 1e-9, max_iter: int = 50, gate_dt=None,
+                  gate_bins: int = 0):
     """Launch the leaf boxes + plan kernels and the asynchronous readback of
     the descriptors (pinned) on the current stream; returns a pending plan
-    for finish_lattices (which is the only host wait)."""
+    for finish_lattices (which is the only host wait).  With ``gate_dt``
+    (profile bin width) and ``gate_bins`` (profile length) the leaf range
+    gate (hhsar_leaf_range_gate) comes back with the plan as lat.gate."""
+    import ctypes
     import torch
     dev = el_dev.device
     stream = _native.stream_handle()
     staged, cuts, n_b = _plan_upload(sched, region)
     up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
     up.copy_(staged, non_blocking=True)
+    if _trace:
+        _trace("plan inputs up")
     descs_dev = up[cuts[0]:cuts[1]]
     bounds = up[cuts[1]:cuts[2]]
     boundary = up[cuts[2]:cuts[3]]
-    status = up[cuts[3]:cuts[4]]  # int32 status, pad, int64 totals[2]
+    status = up[cuts[3]:cuts[4]]  # int32 status, pad, int64 totals[2], int64 gate[2]
     leaf_box = torch.empty((sched.n_leaves, 6), dtype=torch.float64, device=dev)
     _native.call("hhsar_leaf_boxes", _native.ptr(el_dev), _native.ptr(bounds), sched.n_leaves,
                  _native.ptr(leaf_box), stream)
@@ -269,7 +276,13 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     _native.call("hhsar_grid_plan", _native.ptr(descs_dev), sched.n_grids, _native.ptr(leaf_box),
                  _native.ptr(boundary), n_b, _native.ptr(geom), _native.ptr(status),
                  _native.c_void_p_offset(status, 8), stream)
-    back = torch.empty(int(cuts[1]) + 24, dtype=torch.uint8, pin_memory=True)
+    if gate_dt is not None:
+        a, b = sched.level_slices[0]
+        _native.call("hhsar_leaf_range_gate",
+                     ctypes.c_void_p(descs_dev.data_ptr() + a * _native.GRID_DTYPE.itemsize),
+                     b - a, float(gate_dt), int(gate_bins), _native.c_void_p_offset(status, 24),
+                     stream)
+    back = torch.empty(int(cuts[1]) + 40, dtype=torch.uint8, pin_memory=True)
     back[:cuts[1]].copy_(descs_dev, non_blocking=True)
     back[cuts[1]:].copy_(status, non_blocking=True)
     done = torch.cuda.Event()
@@ -298,7 +311,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     if int(status[:4].view(np.int32)[0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
     # offsets, column offsets and both totals came from the plan (device scan)
-    total, n_cols = (int(v) for v in status[8:24].view(np.int64))
+    total, n_cols, g_b0, g_w = (int(v) for v in status[8:40].view(np.int64))
     if newton_grids is not None:
         # Newton work list restricted to the selected grids: re-derive the
         # column offsets and send the descriptors back up
@@ -314,8 +327,11 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     if _trace:
         _trace("worklist built")
     positions = torch.empty((total, 3), dtype=torch.float64, device=dev)
-    valid = torch.zeros(total, dtype=torch.uint8, device=dev)
-    stats = torch.zeros((sched.n_grids, _native.GRID_STATS), dtype=torch.int64, device=dev)
+    # valid flags and per-grid counters zeroed by one fill
+    vb = -(-total // 8) * 8
+    zero = torch.zeros(vb + sched.n_grids * _native.GRID_STATS * 8, dtype=torch.uint8, device=dev)
+    valid = zero[:total]
+    stats = zero[vb:].view(torch.int64).view(sched.n_grids, _native.GRID_STATS)
     if _trace:
         _trace("pools allocated")
     _native.call("hhsar_grid_newton", _native.ptr(descs_dev), sched.n_grids, n_cols,
@@ -323,6 +339,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
                  _native.ptr(stats), stream)
     lat = Lattices(host, descs_dev, positions, valid, stats, geom)
     lat.keep = (p["back"], p["keep"][1])  # pinned staging must outlive the async copy
+    lat.gate = (g_b0, g_w) if g_w > 0 else None
     return lat
 
 
@@ -366,8 +383,8 @@ class Pipeline:
                                   device=self.dev)
         self.lat.values = self.values
         self.n_stages = len(self.sched.fanouts)
-        self.flags = torch.zeros(self.n_stages + 1, dtype=torch.int64, device=self.dev)
-        self.oow = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        counters = torch.zeros(self.n_stages + 2, dtype=torch.int64, device=self.dev)
+        self.flags, self.oow = counters[:self.n_stages + 1], counters[self.n_stages + 1:]
         self.env_ptr = ctypes.c_void_p(env.data_ptr() - int(env_row0) * env.shape[1] * 8)
 
     def leaves(self, g0=None, g1=None):
@@ -464,7 +481,9 @@ def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
     centre) can overhang that by the element box's diagonal, plus 2 bins of
     interpolation/rounding pad on each side.  Only the leaf stage reads
     envelopes (merges read lattices), so profiles outside the gate are never
-    needed: config 4 keeps ~160 of 4,096 bins."""
+    needed: config 4 keeps 288 of 4,096 bins.  Host restatement of
+    hhsar_leaf_range_gate (the step uses the device one, which comes back
+    with the plan; tests check the two agree)."""
     d = lat.descs
     a, b = sched.level_slices[0]
     box = np.asarray(d["box"][a:b], dtype=np.float64)
@@ -499,22 +518,29 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     """
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
+    if _trace:
+        _trace("enter")
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
     window_hi = 0.0 + (n_t - 1) * dt
     main = torch.cuda.current_stream()
     geo = geometry_stream(cube_dev.device)
     geo.wait_stream(main)
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
+    if _trace:
+        _trace("schedule")
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
-                                src_pad_of(params), window_hi)
+                                src_pad_of(params), window_hi,
+                                gate_dt=dt if gate else None, gate_bins=n_t)
     if not gate:
         env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
         t0 = 0.0
     with torch.cuda.stream(geo):
         lat = finish_lattices(pending)
     if gate:
-        b0, w = leaf_range_gate(lat, sched, dt, n_t)
+        b0, w = lat.gate
+        if _trace:
+            _trace("gate")
         env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
     main.wait_stream(geo)
     # blocks allocated on the side stream are used on the main one from here
@@ -522,6 +548,8 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         t.record_stream(main)
     pipe = Pipeline(env, el_dev, el4, t0, dt, k_ref, kgrid, region, final_dims, params, levels,
                     merge_factor, window_hi, sched=sched, lat=lat)
+    if _trace:
+        _trace("pipeline ready")
     return pipe.run(vox_range)
 
 

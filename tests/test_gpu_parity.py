@@ -350,7 +350,7 @@ def test_range_gate_matches_full_profiles(config):
     same image to float rounding, same lattices and flags, no leaf delay
     outside the gated window."""
     import torch
-    from paper_2506_23568_b200 import bpa, ffbp, workloads
+    from paper_2506_23568_b200 import bpa, ffbp, rangecomp, workloads
     w = workloads.config(config)
     gen = torch.Generator(device="cuda").manual_seed(w.seed)
     cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
@@ -368,3 +368,5 @@ def test_range_gate_matches_full_profiles(config):
     assert np.argmax(np.abs(gated)) == np.argmax(np.abs(full))
     assert torch.equal(runs[0].lattices.stats, runs[1].lattices.stats)
     assert torch.equal(runs[0].flags, runs[1].flags)
+    n_t, dt, _, _ = rangecomp.profile_axis(w.freqs, w.upsample)
+    assert runs[1].lattices.gate == ffbp.leaf_range_gate(runs[1].lattices, runs[1].sched, dt, n_t)
