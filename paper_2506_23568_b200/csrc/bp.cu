@@ -77,18 +77,6 @@ struct BpFast {
     double kc_t0;    // k_ref c t0
 };
 
-__device__ __forceinline__ float sqrt_approx(float x) {
-    float r;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-__device__ __forceinline__ float rsqrt_approx(float x) {
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
 template <int VX, int MINB, bool PAIR>
 __global__ void __launch_bounds__(TL_THREADS, MINB)
 bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx, int ny,

@@ -77,6 +77,26 @@ __device__ __forceinline__ bool llt_exact(const double *ext, const hhsar_geom &g
     return !(rad <= xmul(gap, 1e-12));
 }
 
+// ---- single-MUFU fp32 approximations (ftz: no denormal rescaling around
+// the SFU op, which the non-ftz forms add: 3 extra instructions each) ---------
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // ---- SFU-seeded float64 rsqrt / reciprocal --------------------------------------
 // fp32 MUFU seed (relative error < 2^-22) refined by ONE float64 Newton step:
 // relative error ~1.5 e0^2 < 1e-13.  Used where a float64 result feeds a

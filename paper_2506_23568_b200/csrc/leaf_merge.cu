@@ -229,7 +229,7 @@ __device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, co
     return true;
 }
 
-__device__ __forceinline__ float sqrt_fast(float a) { return a * rsqrtf(fmaxf(a, 1e-30f)); }
+__device__ __forceinline__ float sqrt_fast(float a) { return sqrt_approx(a); }
 
 // exp(j phi), float64 phase of any size: reduction by 2 pi with a magic-number
 // round (no FRND), then the fp32 SFU sincos.
@@ -270,8 +270,8 @@ __device__ __forceinline__ bool merge_point(const MergeChild *__restrict__ kids,
         const float dyz = fmaf(dy0, dy0, z2f), dxz = fmaf(dx0, dx0, z2f);
         const float da = sqrt_fast(fmaf(axf, axf, dyz)), db = sqrt_fast(fmaf(bxf, bxf, dyz));
         const float dc = sqrt_fast(fmaf(ayf, ayf, dxz)), dd = sqrt_fast(fmaf(byf, byf, dxz));
-        const float cu = __fdividef(C.ku * (axf + bxf), da + db) + C.ou;
-        const float cv = __fdividef(C.kv * (ayf + byf), dc + dd) + C.ov;
+        const float cu = fmaf(C.ku * (axf + bxf), rcp_approx(da + db), C.ou);
+        const float cv = fmaf(C.kv * (ayf + byf), rcp_approx(dc + dd), C.ov);
         const double ax = x - C.ext[0], bx = x - C.ext[1], ay = y - C.ext[2], by = y - C.ext[3];
         const double xa = ax * ax, xb = bx * bx, ya = ay * ay, yb = by * by;
         const double r = ((sqrt_d(xa + ya + z2) + sqrt_d(xa + yb + z2)) + sqrt_d(xb + ya + z2)) +
@@ -372,8 +372,8 @@ merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, do
             const float dyz = dy02 + z2f[j], dxz = dx02 + z2f[j];
             const float da = sqrt_fast(ax2 + dyz), db = sqrt_fast(bx2 + dyz);
             const float dc = sqrt_fast(ay2 + dxz), dd = sqrt_fast(by2 + dxz);
-            const float cu = __fdividef(nu_, da + db) + C.ou;
-            const float cv = __fdividef(nv_, dc + dd) + C.ov;
+            const float cu = fmaf(nu_, rcp_approx(da + db), C.ou);
+            const float cv = fmaf(nv_, rcp_approx(dc + dd), C.ov);
             const double r = ((sqrt_d(s_aa + z2[j]) + sqrt_d(s_ab + z2[j])) + sqrt_d(s_ba + z2[j])) +
                              sqrt_d(s_bb + z2[j]);
             const double sq = sqrt_d(fma(r, r, -C.gap));
