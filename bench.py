@@ -346,7 +346,11 @@ def hhffbpa_roofline(w, leaf_units, merge_units, newton_iterations, ms, bins_wri
         "merges_and_landing": merge_units * 45 / (64 * sms * clk),
     }
     t_ideal = sum(stages.values())
+    # the same with the range stage's full-profile bytes (the reference's
+    # work: every bin of every envelope), for comparison with ungated runs
+    t_full = t_ideal - stages["range_compression"] + w.n_elements * (w.freqs.count + n_t) * 8 / hbm
     return {"t_ideal_ms": round(t_ideal * 1e3, 3), "frac": round(t_ideal * 1e3 / ms, 3),
+            "frac_vs_full_profiles": round(t_full * 1e3 / ms, 3),
             "stages_ms": {k: round(v * 1e3, 3) for k, v in stages.items()},
             "method": "SURVEY 8(d): sum over stages of work / bounding-unit peak (HBM "
                       "MEASURED_PEAKS.json; MUFU 16, FP64 64 lanes/clk/SM at the max clock)"}

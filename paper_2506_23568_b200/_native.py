@@ -169,9 +169,8 @@ def simulate(elements, positions, refl, k_samples, device="cuda"):
     """Born cube on the device (hhsar_simulate); returns a complex64 tensor."""
     import torch
     library()
-    el = torch.as_tensor(np.ascontiguousarray(elements, dtype=np.float64), device=device)
-    pos = torch.as_tensor(np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3),
-                          device=device)
+    el = torch.tensor(np.asarray(elements, dtype=np.float64), device=device)
+    pos = torch.tensor(np.asarray(positions, dtype=np.float64).reshape(-1, 3), device=device)
     r = np.ascontiguousarray(np.asarray(refl, dtype=np.complex128))
     rr = torch.as_tensor(r.view(np.float64), device=device)
     k = torch.as_tensor(np.ascontiguousarray(k_samples, dtype=np.float64), device=device)

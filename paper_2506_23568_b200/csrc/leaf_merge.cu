@@ -166,8 +166,12 @@ __device__ __forceinline__ void split_f(float c, float hi, int &i, float &f) {
 __device__ __forceinline__ void split_d(double c, int hi, int &i, float &f) {
     const double magic = 6755399441055744.0;  // 1.5 * 2^52
     const double t = __dadd_rd(c, magic);
-    i = min(__double2loint(t), hi);
-    f = (float)(c - (double)i);
+    i = __double2loint(t);
+    f = (float)(c - (t - magic));  // exact floor, no int -> double conversion
+    if (i > hi) {  // c at the top edge: base hi, fraction 1
+        i = hi;
+        f += 1.f;
+    }
 }
 
 // Lattice interpolation with the reference's hull rules (_kernels.py:117-189)
@@ -189,21 +193,22 @@ __device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, co
     const float2 *base = vals + C.offset;
     float2 acc = make_float2(0.f, 0.f);
     if (KERNEL == 0) {
+        // trilinear as nested lerps along n, v, u on (re, im) pairs: one
+        // FADD2 + one FFMA2 per lerp, no weight products
         const float2 *b = base + ((iu * C.nv + iv) * C.nn + iw);
-        f2x a2 = pk2(0.f, 0.f);  // (re, im) accumulated with FFMA2, scalar weights broadcast
+        f2x r[2][2];
 #pragma unroll
-        for (int a = 0; a < 2; ++a) {
-            const float wa = a ? fu : 1.f - fu;
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int bb = 0; bb < 2; ++bb) {
-                const float wb = bb ? fv : 1.f - fv;
                 const float2 *row = b + a * su + bb * C.nn;
                 const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
-                const float w0 = wa * wb * (1.f - fn), w1 = wa * wb * fn;
-                a2 = fma2(pk2(v1.x, v1.y), bc2(w1), a2);
-                a2 = fma2(pk2(v0.x, v0.y), bc2(w0), a2);
+                const f2x x0 = pk2(v0.x, v0.y);
+                r[a][bb] = fma2(bc2(fn), sub2(pk2(v1.x, v1.y), x0), x0);
             }
-        }
+        const f2x s0 = fma2(bc2(fv), sub2(r[0][1], r[0][0]), r[0][0]);
+        const f2x s1 = fma2(bc2(fv), sub2(r[1][1], r[1][0]), r[1][0]);
+        const f2x a2 = fma2(bc2(fu), sub2(s1, s0), s0);
         acc = make_float2(lo2(a2), hi2(a2));
     } else {
         float wu[4], wv[4], wn[4];
