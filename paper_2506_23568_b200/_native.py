@@ -17,7 +17,9 @@ import numpy as np
 from .errors import NativeUnavailableError
 
 LIB_NAME = "libhhsar_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+# HHSAR_LIB overrides the in-tree library (A/B builds in tools/, never set
+# by the tests or the bench)
+LIB_PATH = Path(os.environ.get("HHSAR_LIB") or Path(__file__).resolve().parent / LIB_NAME)
 
 # numpy mirrors of the C structs (align=True follows the C layout rules;
 # checked against hhsar_abi_layout() at load time)
@@ -87,7 +89,11 @@ def library(require_gpu: bool = True):
                 "(make -C paper_2506_23568_b200/csrc)")
         lib = ctypes.CDLL(str(LIB_PATH))
         for name, (args, res) in SIGNATURES.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None and os.environ.get("HHSAR_LIB"):
+                continue  # an older A/B build
+            if fn is None:
+                raise NativeUnavailableError(f"{LIB_PATH} does not export {name}")
             fn.argtypes = args
             fn.restype = res
         _check_layout(lib)

@@ -161,6 +161,11 @@ __device__ __forceinline__ void idft(float2 (&v)[R]) {
 }
 
 __device__ __forceinline__ int rc_pad(int i) { return i + (i >> 4); }  // breaks stride-16 bank conflicts
+// Every shared-memory access of a pass is x0 + r s (r < R, compile-time
+// stride s) with (x0 mod 16) + (r s mod 16) < 16 -- s a multiple of 16, or s
+// a power of two below 16 with x0 mod s = 0 -- so rc_pad(x0 + r s) =
+// rc_pad(x0) + r s + (r s >> 4): one address register per pass and
+// immediate offsets (no per-access shift/add/LEA).
 
 template <int LOGN>
 struct RcShape {
@@ -238,8 +243,9 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         if constexpr (S::REM == 0 && P16 == 1) {
             emit(j, v);
         } else {
+            float2 *q = buf + rc_pad(j * R0);
 #pragma unroll
-            for (int r = 0; r < R0; ++r) buf[rc_pad(j * R0 + r)] = v[r];
+            for (int r = 0; r < R0; ++r) q[r] = v[r];
         }
     }
     if constexpr (S::REM == 0 && P16 == 1) return;
@@ -259,7 +265,8 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
         }
         float2 v[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = buf[rc_pad(j + r * T)];
+        for (int r = 0; r < 16; ++r)
+            v[r] = (T % 16 == 0) ? buf[rc_pad(j) + r * T + ((r * T) >> 4)] : buf[rc_pad(j + r * T)];
         if (gated && p == P16 - 1) {
             // the few outputs i = j + r T this thread owns: y = sum_q v[q] z^q
             // with z = e^{2 pi i i / N} = w (e^{2 pi i / 16})^r, evaluated as
@@ -303,7 +310,7 @@ range_compress_kernel(const float2 *__restrict__ cube, int64_t n_el, int n_f,
             __syncthreads();  // every read of this pass precedes any write
             const int base = (j - k) * 16 + k;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) buf[rc_pad(base + r * ns)] = v[r];
+            for (int r = 0; r < 16; ++r) buf[rc_pad(base) + r * ns + ((r * ns) >> 4)] = v[r];
             __syncthreads();
         }
         ns *= 16;
