@@ -185,61 +185,76 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
             s_env[q] = make_float4(a.x, a.y, b2.x, b2.y);
         }
         __syncthreads();
-        for (int j = 0; j < cn; ++j) {
-            const float4 e = s_el[j];
-            const int offb = __float_as_int(e.w);
-            if (offb != -1) {
-                const unsigned base = (unsigned)offb;
-                const f2x nex = bc2(-e.x), ney = bc2(-e.y), nez = bc2(-e.z);
+        // one element against this thread's P points: the fast (staged) unit
+        auto fast_unit = [&](const float4 &e) {
+            const unsigned base = (unsigned)__float_as_int(e.w);
+            const f2x nex = bc2(-e.x), ney = bc2(-e.y), nez = bc2(-e.z);
 #pragma unroll
-                for (int q = 0; q < P; q += 2) {
-                    const f2x dx = add2(pk2(px[q], px[q + 1]), nex);
-                    const f2x dy = add2(pk2(py[q], py[q + 1]), ney);
-                    const f2x dz = add2(pk2(pz[q], pz[q + 1]), nez);
-                    const f2x a2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-                    const f2x d = pk2(lp_sqrt(lo2(a2)), lp_sqrt(hi2(a2)));
-                    const f2x tb = add2(fma2(d, bc2(k.inv_bin), bc2(k.cbin)), bc2(LP_MAGIC));
-                    const f2x f = fma2(d, bc2(k.inv_bin), sub2(bc2(k.kfrac), tb));
-                    const unsigned i0 = (unsigned)__float_as_int(lo2(tb)) * 16u + base;
-                    const unsigned i1 = (unsigned)__float_as_int(hi2(tb)) * 16u + base;
-                    const float4 w0 =
-                        *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(s_env) + i0);
-                    const float4 w1 =
-                        *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(s_env) + i1);
-                    const f2x v0 = fma2(bc2(lo2(f)), pk2(w0.z, w0.w), pk2(w0.x, w0.y));
-                    const f2x v1 = fma2(bc2(hi2(f)), pk2(w1.z, w1.w), pk2(w1.x, w1.y));
-                    const f2x ang = mul2(f, bc2(k.alpha));
-                    float s0, cs0, s1, cs1;
-                    __sincosf(lo2(ang), &s0, &cs0);
-                    __sincosf(hi2(ang), &s1, &cs1);
-                    pa[q] = fma2(v0, bc2(cs0), pa[q]);
-                    pb[q] = fma2(v0, bc2(s0), pb[q]);
-                    pa[q + 1] = fma2(v1, bc2(cs1), pa[q + 1]);
-                    pb[q + 1] = fma2(v1, bc2(s1), pb[q + 1]);
-                }
-            } else {
-                if (t == 0) atomicAdd(&g_leaf_checked, 1ull);
-                // checked path: exact reference skip-and-count, global gathers
-                const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
-#pragma unroll
-                for (int q = 0; q < P; ++q) {
-                    const float dx = px[q] - e.x, dy = py[q] - e.y, dz = pz[q] - e.z;
-                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    const float x = fmaf(d, k.inv_bin, -k.x0);
-                    if (!(x >= 0.f && x <= k.xmax)) {
-                        bad += lat[q] >= 0;
-                        continue;
-                    }
-                    const int ib = min((int)x, k.n_t - 2);
-                    const float fr = x - (float)ib;
-                    const float2 u0 = __ldg(row + ib), u1 = __ldg(row + ib + 1);
-                    const float er = fmaf(fr, u1.x - u0.x, u0.x), ei = fmaf(fr, u1.y - u0.y, u0.y);
-                    const float rv = d * k.rev;
-                    float s, cs;
-                    __sincosf(6.283185307f * __fsub_rn(rv, rintf(rv)), &s, &cs);
-                    pa[q] = add2(pa[q], pk2(er * cs - ei * s, er * s + ei * cs));
-                }
+            for (int q = 0; q < P; q += 2) {
+                const f2x dx = add2(pk2(px[q], px[q + 1]), nex);
+                const f2x dy = add2(pk2(py[q], py[q + 1]), ney);
+                const f2x dz = add2(pk2(pz[q], pz[q + 1]), nez);
+                const f2x a2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+                const f2x d = pk2(lp_sqrt(lo2(a2)), lp_sqrt(hi2(a2)));
+                const f2x tb = add2(fma2(d, bc2(k.inv_bin), bc2(k.cbin)), bc2(LP_MAGIC));
+                const f2x f = fma2(d, bc2(k.inv_bin), sub2(bc2(k.kfrac), tb));
+                const unsigned i0 = (unsigned)__float_as_int(lo2(tb)) * 16u + base;
+                const unsigned i1 = (unsigned)__float_as_int(hi2(tb)) * 16u + base;
+                const float4 w0 =
+                    *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(s_env) + i0);
+                const float4 w1 =
+                    *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(s_env) + i1);
+                const f2x v0 = fma2(bc2(lo2(f)), pk2(w0.z, w0.w), pk2(w0.x, w0.y));
+                const f2x v1 = fma2(bc2(hi2(f)), pk2(w1.z, w1.w), pk2(w1.x, w1.y));
+                const f2x ang = mul2(f, bc2(k.alpha));
+                float s0, cs0, s1, cs1;
+                __sincosf(lo2(ang), &s0, &cs0);
+                __sincosf(hi2(ang), &s1, &cs1);
+                pa[q] = fma2(v0, bc2(cs0), pa[q]);
+                pb[q] = fma2(v0, bc2(s0), pb[q]);
+                pa[q + 1] = fma2(v1, bc2(cs1), pa[q + 1]);
+                pb[q + 1] = fma2(v1, bc2(s1), pb[q + 1]);
             }
+        };
+        // checked path: exact reference skip-and-count, global gathers
+        auto checked_unit = [&](const float4 &e, int j) {
+            if (t == 0) atomicAdd(&g_leaf_checked, 1ull);
+            const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const float dx = px[q] - e.x, dy = py[q] - e.y, dz = pz[q] - e.z;
+                const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                const float x = fmaf(d, k.inv_bin, -k.x0);
+                if (!(x >= 0.f && x <= k.xmax)) {
+                    bad += lat[q] >= 0;
+                    continue;
+                }
+                const int ib = min((int)x, k.n_t - 2);
+                const float fr = x - (float)ib;
+                const float2 u0 = __ldg(row + ib), u1 = __ldg(row + ib + 1);
+                const float er = fmaf(fr, u1.x - u0.x, u0.x), ei = fmaf(fr, u1.y - u0.y, u0.y);
+                const float rv = d * k.rev;
+                float s, cs;
+                __sincosf(6.283185307f * __fsub_rn(rv, rintf(rv)), &s, &cs);
+                pa[q] = add2(pa[q], pk2(er * cs - ei * s, er * s + ei * cs));
+            }
+        };
+        // elements two at a time (loop overhead and the element load shared;
+        // two independent unit chains in flight)
+        int j = 0;
+        for (; j + 1 < cn; j += 2) {
+            const float4 ea = s_el[j], eb = s_el[j + 1];
+            if (__float_as_int(ea.w) != -1 && __float_as_int(eb.w) != -1) {
+                fast_unit(ea);
+                fast_unit(eb);
+            } else {
+                if (__float_as_int(ea.w) != -1) fast_unit(ea); else checked_unit(ea, j);
+                if (__float_as_int(eb.w) != -1) fast_unit(eb); else checked_unit(eb, j + 1);
+            }
+        }
+        if (j < cn) {
+            const float4 e = s_el[j];
+            if (__float_as_int(e.w) != -1) fast_unit(e); else checked_unit(e, j);
         }
     }
     const double gap = box_gap_exact(D.ext);
