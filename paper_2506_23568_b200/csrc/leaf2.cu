@@ -60,6 +60,7 @@ compact_leaf_kernel(const hhsar_grid_desc *__restrict__ grids, const uint8_t *__
 }
 
 __device__ unsigned long long g_leaf_checked;  // (CTA, element) pairs on the checked path
+__device__ unsigned long long g_leaf_tw[4];    // CTAs per window width 32 / 64 / 128 / 256
 
 // Carrier rotation per delay bin, exp(j k_ref c (t0 + dt bin)), float64 phase
 // reduced then rounded once: shared by every element's window staging.
@@ -94,7 +95,8 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     const int p0 = chunk * LP_THREADS * P;
     if (p0 >= n) return;  // block-uniform
     const int t = threadIdx.x;
-    // my points (strided so a warp's loads are contiguous)
+    // my points: P consecutive list entries per thread, so a partial last
+    // chunk leaves whole warps without points (they skip the unit loop)
     float px[P], py[P], pz[P];
     int lat[P];
     // leaf centre (element bbox midpoint) and the chunk's range shell around it
@@ -103,7 +105,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     float dmin = 3e38f, dmax = 0.f;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-        const int li = p0 + q * LP_THREADS + t;
+        const int li = p0 + P * t + q;
         lat[q] = li < n ? idx[D.offset + li] : -1;
         const int src = lat[q] >= 0 ? lat[q] : idx[D.offset + p0];  // dead lanes mirror a live point
         const double *pp = positions + 3 * (D.offset + src);
@@ -115,6 +117,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         dmin = fminf(dmin, dc);
         dmax = fmaxf(dmax, dc);
     }
+    const bool warp_live = __any_sync(0xffffffffu, lat[0] >= 0);
     for (int o = 16; o > 0; o >>= 1) {
         dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -148,6 +151,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __syncthreads();
     for (int w = 0; w < LP_THREADS / 32; ++w) need = max(need, __float_as_int(s_box[0][w]));
     const int lw = need <= 32 ? 5 : need <= 64 ? 6 : need <= 128 ? 7 : 8;  // log2 TW
+    if (t == 0) atomicAdd(&g_leaf_tw[lw - 5], 1ull);
     const int TW = 1 << lw, LP_CHUNK = WIN >> lw;
     f2x pa[P], pb[P];
 #pragma unroll
@@ -241,7 +245,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         };
         // elements two at a time (loop overhead and the element load shared;
         // two independent unit chains in flight)
-        int j = 0;
+        int j = warp_live ? 0 : cn;  // warps without points only stage
         for (; j + 1 < cn; j += 2) {
             const float4 ea = s_el[j], eb = s_el[j + 1];
             if (__float_as_int(ea.w) != -1 && __float_as_int(eb.w) != -1) {
@@ -319,4 +323,12 @@ extern "C" unsigned long long hhsar_debug_leaf_checked(void) {
     cudaMemcpyFromSymbol(&v, hhsar::g_leaf_checked, sizeof(v));
     cudaMemcpyToSymbol(hhsar::g_leaf_checked, &z, sizeof(z));
     return v;
+}
+
+// Diagnostics: CTAs per staged window width (32, 64, 128, 256 bins) since
+// the last call, into out[4].
+extern "C" void hhsar_debug_leaf_tw(unsigned long long *out) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyFromSymbol(out, hhsar::g_leaf_tw, sizeof(z));
+    cudaMemcpyToSymbol(hhsar::g_leaf_tw, z, sizeof(z));
 }

@@ -37,14 +37,23 @@ for tw in ["auto"]:
 
     _native.call = timed
     vols = []
+    tw_hist = (ctypes.c_ulonglong * 4)()
     for rep in range(3):
         lib.hhsar_debug_leaf_checked()
+        lib.hhsar_debug_leaf_tw(tw_hist)
         run = ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params, w.levels,
                                      w.merge_factor, w.upsample)
         torch.cuda.synchronize()
         checked = lib.hhsar_debug_leaf_checked()
+        lib.hhsar_debug_leaf_tw(tw_hist)
         vols.append(run.volume)
     _native.call = orig
     ms = min(s.elapsed_time(e) for s, e in times)
+    a, b = run.sched.level_slices[0]
+    d = run.lattices.descs
+    m = (d["stop"][a:b] - d["start"][a:b]).astype(np.int64)
+    pts = run.lattices.stats[a:b, 2].cpu().numpy()
+    print(f"CTAs per window width 32/64/128/256: {list(tw_hist)}; leaves {b - a}, elements "
+          f"per leaf {m.mean():.0f}, points per leaf {pts.mean():.0f}")
     print(f"TW {tw}: leaf {ms:.3f} ms, checked pairs {checked}, "
           f"volume norm {torch.linalg.norm(vols[-1]).item():.6e}", flush=True)
