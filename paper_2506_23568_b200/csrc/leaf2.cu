@@ -88,6 +88,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __shared__ float4 s_env[WIN];
     __shared__ float4 s_el[WIN / 32];
     __shared__ int s_lo[WIN / 32];
+    __shared__ int64_t s_row[WIN / 32];
     __shared__ float s_box[2][LP_THREADS / 32];
     const int gi = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
     const hhsar_grid_desc &D = grids[gi];
@@ -142,7 +143,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         const float re = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
         const float xlo = fmaxf(dmin - re, 0.f) * k.inv_bin - k.x0;
         const float xhi = (dmax + re) * k.inv_bin - k.x0;
-        if (xlo >= 1.f && xhi <= k.xmax - 1.f)
+        if (xlo >= 1.f && xhi <= k.xmax - 2.f)
             need = max(need, min((int)floorf(xhi) + 2, k.n_t - 1) - max((int)floorf(xlo) - 2, 0) + 1);
     }
     need = __reduce_max_sync(0xffffffffu, need);
@@ -169,23 +170,26 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
             const float xhi = (dmax + re) * k.inv_bin - k.x0;
             const int lo = max((int)floorf(xlo) - 2, 0);
             const int hi = min((int)floorf(xhi) + 2, k.n_t - 1);
-            const bool fast = xlo >= 1.f && xhi <= k.xmax - 1.f && hi - lo + 1 <= TW;
-            const unsigned off = (unsigned)(t * TW - lo) * 16u - LP_MAGIC_BITS * 16u;
+            // staged bins [lo', lo' + TW) with lo' + TW <= n_t - 1, so every
+            // staged bin has a successor (no clamps below); the window still
+            // covers every unit's base bin, with a bin of rounding margin
+            const int los = min(lo, k.n_t - 1 - TW);
+            const bool fast = xlo >= 1.f && xhi <= k.xmax - 2.f && hi - lo + 1 <= TW && los >= 0;
+            const unsigned off = (unsigned)(t * TW - los) * 16u - LP_MAGIC_BITS * 16u;
             s_el[t] = make_float4(e.x, e.y, e.z, __int_as_float(fast ? (int)off : -1));
-            s_lo[t] = fast ? lo : -1;
+            s_lo[t] = fast ? los : -1;
+            s_row[t] = (e0 + c0 + t) * (int64_t)k.n_t;
         }
         __syncthreads();
+#pragma unroll 2
         for (int q = t; q < cn * TW; q += LP_THREADS) {
             const int j = q >> lw, lo = s_lo[j];
             if (lo < 0) continue;
             const int bin = lo + (q & (TW - 1));
-            const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
-            const float2 v0 = __ldg(row + min(bin, k.n_t - 1));
-            const float2 v1 = __ldg(row + min(bin + 1, k.n_t - 1));
+            const float2 *row = env + (s_row[j] + bin);
+            const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
             const float2 r = __ldg(rot + bin);
-            const float2 dv = bin < k.n_t - 1 ? make_float2(v1.x - v0.x, v1.y - v0.y)
-                                              : make_float2(0.f, 0.f);
-            const float2 a = cmul(v0, r), b2 = cmul(dv, r);
+            const float2 a = cmul(v0, r), b2 = cmul(make_float2(v1.x - v0.x, v1.y - v0.y), r);
             s_env[q] = make_float4(a.x, a.y, b2.x, b2.y);
         }
         __syncthreads();
