@@ -323,9 +323,8 @@ merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, i
 // Cartesian landing, ZQ consecutive z voxels of one (x, y) column per
 // thread: the child constants and every x/y-only term (lateral offsets,
 // their squares, the clamped u/v offsets) are computed once for the ZQ
-// voxels; the per-voxel work is the same merge_point arithmetic.  ZQ = 4
-// with >= 4 children (config 4: 5.3 -> 4.9 ms), 2 otherwise (config 3:
-// 0.69 -> 0.66 ms; 4 would be 0.72).
+// voxels; the per-voxel work is the same merge_point arithmetic.  ZQ = 4 or
+// 2, chosen at launch (hhsar_merge_cartesian).
 template <int KERNEL, int ZQ>
 __global__ void __launch_bounds__(MERGE_THREADS)
 merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx,
@@ -548,7 +547,10 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
                                               vox_begin, vox_end, q0, q1 - q0, kids,
                                               (int)n_children, kv, *geom, o, flagged);
     };
-    const bool wide = n_children >= 4;
+    // 4 z-voxels per thread when there are >= 4 children or the launch is
+    // large (config 4, 268 M voxels x 2 children: 4.49 -> 4.19 ms); 2
+    // otherwise (config 3, 33.5 M voxels: 0.61 ms vs 0.62)
+    const bool wide = n_children >= 4 || vox_end - vox_begin >= (int64_t(1) << 26);
     if (kernel == 0) {
         if (wide) launch(merge_cartesian_kernel<0, 4>, 4);
         else launch(merge_cartesian_kernel<0, 2>, 2);
