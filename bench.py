@@ -24,6 +24,7 @@ host cores) on a bounded voxel sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -431,13 +432,14 @@ def hhffbpa_leg(index, dev, steps, check=False):
     for _ in range(3):
         run = step()
     torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(steps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record()
+    for i in range(steps):
         run = step()
-    t1.record()
+        ev[i + 1].record()
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / steps
+    ms = ev[0].elapsed_time(ev[-1]) / steps
+    per_step = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
     stats = run.lattices.stats.cpu().numpy()
     sched, d = run.sched, run.lattices.descs
     g0, g1 = sched.level_slices[0]
@@ -452,6 +454,8 @@ def hhffbpa_leg(index, dev, steps, check=False):
                        f"freqs, {list(w.dims)} voxels, {sched_name}"
                        + (", seeded random cube" if big else ""),
            "ms_per_step": round(ms, 3), "volumes_per_s": round(1e3 / ms, 2),
+           "step_ms_min_median_max": [round(per_step[0], 3), round(per_step[len(per_step) // 2], 3),
+                                      round(per_step[-1], 3)],
            "bpa_equivalent_gunits_per_s": round(w.bpa_units / (ms / 1e3) / 1e9, 1),
            "grids": int(sched.n_grids), "leaf_units": leaf_units, "merge_units": merge_units,
            "newton_iterations": int(stats[:, 4].sum()),
@@ -608,6 +612,10 @@ def main():
                     help="reference arm: y-rows (x 64 z-voxels) of one x-plane per step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    # no cyclic-GC pauses inside the timed regions (reference counting still
+    # frees every per-step buffer); the process is short-lived
+    gc.collect()
+    gc.disable()
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
     if res is not None:
         print(json.dumps(res))
