@@ -381,19 +381,27 @@ __device__ __forceinline__ void finish_plane(const hhsar_grid_desc &D, const hhs
                                              bool ok, double x, double y, double z, bool core_uv,
                                              int64_t base, uint8_t *__restrict__ valid,
                                              double *__restrict__ positions, unsigned (&acc)[6]) {
-    if (w < D.near_lo[2]) return;
-    const bool pre = ok && x >= D.slack_lo[0] && x <= D.slack_hi[0] && y >= D.slack_lo[1] &&
-                     y <= D.slack_hi[1] && z >= D.slack_lo[2] && z <= D.slack_hi[2];
+    // every descriptor field this needs is loaded up front (independent
+    // loads in flight together; no short-circuit chain of dependent loads)
+    const int near_lo = D.near_lo[2], is_leaf = D.is_leaf, core_lo = D.core_lo[2],
+              core_hi = D.core_hi[2];
+    const double sl0 = D.slack_lo[0], sl1 = D.slack_lo[1], sl2 = D.slack_lo[2];
+    const double sh0 = D.slack_hi[0], sh1 = D.slack_hi[1], sh2 = D.slack_hi[2];
+    const double b0 = D.box[0], b1 = D.box[1], b2 = D.box[2], b3 = D.box[3], b4 = D.box[4],
+                 b5 = D.box[5];
+    if (w < near_lo) return;
+    const bool pre = ok & (x >= sl0) & (x <= sh0) & (y >= sl1) & (y <= sh1) & (z >= sl2) &
+                     (z <= sh2);
     bool post = pre;
-    if (pre && D.is_leaf) {
+    if (pre && is_leaf) {
         // 2 * max corner distance / c <= window_hi (ffbp.py:320-330).  The
         // farthest of the 8 corners takes, per axis, the bound farther from
         // the point; rounded subtraction, squaring, addition and sqrt are all
         // monotone, so its rounded distance IS the reference's max over the 8
         // (bit-exact, 1 sqrt not 8).
-        const double ex0 = xsub(x, D.box[0]), ex1 = xsub(x, D.box[3]);
-        const double ey0 = xsub(y, D.box[1]), ey1 = xsub(y, D.box[4]);
-        const double ez0 = xsub(z, D.box[2]), ez1 = xsub(z, D.box[5]);
+        const double ex0 = xsub(x, b0), ex1 = xsub(x, b3);
+        const double ey0 = xsub(y, b1), ey1 = xsub(y, b4);
+        const double ez0 = xsub(z, b2), ez1 = xsub(z, b5);
         const double fx = fabs(ex0) >= fabs(ex1) ? ex0 : ex1;
         const double fy = fabs(ey0) >= fabs(ey1) ? ey0 : ey1;
         const double fz = fabs(ez0) >= fabs(ez1) ? ez0 : ez1;
@@ -411,7 +419,7 @@ __device__ __forceinline__ void finish_plane(const hhsar_grid_desc &D, const hhs
             post = xdiv(xmul(2.0, dmax), HHSAR_C_LIGHT) <= g.window_hi;
         }
     }
-    const bool in_core = core_uv && w >= D.core_lo[2] && w <= D.core_hi[2];
+    const bool in_core = core_uv & (w >= core_lo) & (w <= core_hi);
     acc[0] += pre;
     acc[1] += pre && in_core;
     acc[2] += post;
