@@ -15,6 +15,8 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace hhsar {
 
 constexpr int PLAN_THREADS = 128;
@@ -289,6 +291,7 @@ grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__
 //   a fix-up pass in the reference's order (below).
 constexpr int NEWTON_THREADS = 128;
 constexpr int HEAVY_MAXP = 64;  // planes per heavy column held in shared memory
+constexpr int64_t NEWTON_SPEC2_MAX_COLS = 131072;  // speculative continuations up to this size
 
 __device__ __forceinline__ int grid_of_column(const hhsar_grid_desc *__restrict__ grids,
                                               int n_grids, const int32_t *__restrict__ block_grid,
@@ -484,17 +487,26 @@ __global__ void grid_newton_heavy_list_kernel(const hhsar_grid_desc *__restrict_
     if (h) heavy[b0 + __popc(m & ((1u << lane) - 1u))] = (int32_t)c;
 }
 
+// SPEC2 (heavy phase, small problems): a heavy plane whose centre start
+// converged goes on to solve the NEXT plane warm-started from it and stores
+// that in spec2_* (slot [heavy index][plane]) -- exactly the solve the fix-up
+// would run when that centre-started plane is the one the reference
+// converged on, so the fix-up's chain shrinks to runs of >= 2 converged
+// planes.
+template <bool SPEC2>
 __global__ void __launch_bounds__(NEWTON_THREADS)
 grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
                    const int32_t *__restrict__ block_grid, hhsar_geom g,
                    double *__restrict__ positions, uint8_t *__restrict__ valid,
                    int64_t *__restrict__ stats, unsigned long long *__restrict__ counter,
                    const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ n_heavy_p,
-                   int phase, const int32_t *__restrict__ col_grid) {
+                   int phase, const int32_t *__restrict__ col_grid, double *__restrict__ spec2_pos,
+                   uint8_t *__restrict__ spec2_code, int64_t spec2_cap) {
     NewtonGeom G;
     int gi = -1, acc_gi = -1, w = 0, w_end = 0, it = 0, iu = 0, iv = 0;
     int64_t base = 0;  // lattice index of plane 0 of the current column
-    bool have = false, core_uv = false, spec = false;
+    bool have = false, core_uv = false, spec = false, warm2 = false;
+    int64_t hslot = 0;  // SPEC2: heavy index * HEAVY_MAXP
     double tu = 0, tv = 0, tn = 0, x = 0, y = 0, z = 0;
     const double max_step2 = g.max_step * g.max_step;
     // phase 0: heavy (column, plane) slots only; phase 1: light columns only
@@ -525,6 +537,12 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                 w = (int)(t % HEAVY_MAXP);
                 if (w >= wend_col) continue;
                 w_end = w + 1;
+                if constexpr (SPEC2) {
+                    hslot = (int64_t)(t / HEAVY_MAXP) * HEAVY_MAXP;
+                    warm2 = false;
+                    // the warm continuation needs the next plane and a slot
+                    if (w + 1 < wend_col && (int64_t)(t / HEAVY_MAXP) < spec2_cap) w_end = w + 2;
+                }
             } else {
                 w = 0;
                 w_end = wend_col;
@@ -554,11 +572,26 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         const hhsar_grid_desc &D = grids[gi];
         const bool ok = st == 1;
         if (spec) {  // speculative: the fix-up kernel decides
+            if (SPEC2 && warm2) {
+                spec2_code[hslot + w] = spec_code(ok, it);
+                double *pp = spec2_pos + 3 * (hslot + w);
+                pp[0] = x;
+                pp[1] = y;
+                pp[2] = z;
+                have = false;
+                continue;
+            }
             valid[base + w] = spec_code(ok, it);
             double *pp = positions + 3 * (base + w);
             pp[0] = x;
             pp[1] = y;
             pp[2] = z;
+            if (SPEC2 && ok && w + 1 < w_end) {  // continue warm on the next plane
+                warm2 = true;
+                ++w;
+                start_plane(D, x, y, z);
+                continue;
+            }
             have = false;
             continue;
         }
@@ -584,7 +617,9 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
                          double *__restrict__ positions, uint8_t *__restrict__ valid,
                          int64_t *__restrict__ stats, const int32_t *__restrict__ heavy,
                          const unsigned long long *__restrict__ n_heavy_p,
-                         const int32_t *__restrict__ col_grid) {
+                         const int32_t *__restrict__ col_grid,
+                         const double *__restrict__ spec2_pos,
+                         const uint8_t *__restrict__ spec2_code, int64_t spec2_cap) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)*n_heavy_p) return;
     const unsigned long long c = (unsigned long long)heavy[i];
@@ -597,20 +632,32 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
     const bool core_uv = q.iu >= D.core_lo[0] && q.iu <= D.core_hi[0] && q.iv >= D.core_lo[1] &&
                          q.iv <= D.core_hi[1];
     unsigned acc[6] = {0, 0, 0, 0, 0, 0};
-    bool prev_ok = false;
+    bool prev_ok = false, prev_cold = true;
     double px = 0, py = 0, pz = 0;
+    const bool has2 = spec2_code != nullptr && i < spec2_cap;
     for (int w = 0; w < w_end; ++w) {
         const uint8_t code = valid[base + w];
         double *pp = positions + 3 * (base + w);
         bool ok;
         int it;
         double x, y, z;
-        if (!prev_ok) {  // the reference also started this plane from the centre
+        const bool cold = !prev_ok;
+        const uint8_t code2 = (has2 && !cold && prev_cold) ? spec2_code[i * HEAVY_MAXP + w] : 0xff;
+        if (cold) {  // the reference also started this plane from the centre
             ok = code & 0x80;
             it = code & 0x7f;
             x = pp[0];
             y = pp[1];
             z = pp[2];
+        } else if (code2 != 0xff) {
+            // predecessor = its centre start, whose warm continuation the
+            // heavy phase already solved
+            ok = code2 & 0x80;
+            it = code2 & 0x7f;
+            const double *q = spec2_pos + 3 * (i * HEAVY_MAXP + w);
+            x = q[0];
+            y = q[1];
+            z = q[2];
         } else {  // warm start from the converged predecessor
             x = px;
             y = py;
@@ -622,6 +669,7 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
         acc[5] += 1;
         finish_plane(D, g, w, ok, x, y, z, core_uv, base, valid, positions, acc);
         prev_ok = ok;
+        prev_cold = cold;
         px = x;
         py = y;
         pz = z;
@@ -828,29 +876,52 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
     if (n_cols == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
-    static int per_sm = 0;
+    static int per_sm = 0, per_sm2 = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_newton_kernel, NEWTON_THREADS,
-                                                      0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_newton_kernel<false>,
+                                                      NEWTON_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, grid_newton_kernel<true>,
+                                                      NEWTON_THREADS, 0);
         if (per_sm <= 0) per_sm = 1;
+        if (per_sm2 <= 0) per_sm2 = 1;
     }
-    // scratch: [0] work counter, [1] heavy-column count, then the heavy list
+    // Speculative warm continuations of the heavy planes (SPEC2) pay where
+    // the in-order fix-up is the critical path, i.e. small problems (config
+    // 2: 39 k columns); on large ones the heavy phase is throughput work
+    // competing with the range compression, and they are off.
+    static const int spec2_env = [] {
+        const char *e = getenv("HHSAR_NEWTON_SPEC2");
+        return e ? atoi(e) : -1;
+    }();
+    const bool spec2 = spec2_env >= 0 ? spec2_env != 0 : n_cols <= NEWTON_SPEC2_MAX_COLS;
+    const int64_t cap = spec2 ? (n_cols / 8 > 256 ? n_cols / 8 : 256) : 0;  // heavy columns with slots
+    // scratch: [0] work counter, [1] heavy-column count, then the heavy list,
+    // the column -> grid map, and (SPEC2) the continuation slots
     unsigned long long *counter = nullptr;
-    if (cudaMallocAsync(&counter, 2 * sizeof(unsigned long long) + 2 * n_cols * sizeof(int32_t),
-                        s) != cudaSuccess)
+    const size_t head = 2 * sizeof(unsigned long long) + 2 * n_cols * sizeof(int32_t);
+    const size_t slots = (size_t)cap * HEAVY_MAXP;
+    if (cudaMallocAsync(&counter, head + slots * (3 * sizeof(double) + 1), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "grid_newton: scratch allocation failed");
     cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), s);
     int32_t *heavy = reinterpret_cast<int32_t *>(counter + 2);
     int32_t *col_grid = heavy + n_cols;
+    double *spec2_pos = spec2 ? reinterpret_cast<double *>(col_grid + n_cols) : nullptr;
+    uint8_t *spec2_code = spec2 ? reinterpret_cast<uint8_t *>(spec2_pos + 3 * slots) : nullptr;
+    if (spec2) cudaMemsetAsync(spec2_code, 0xff, slots, s);  // 0xff = no continuation
     grid_newton_heavy_list_kernel<<<(unsigned)((n_cols + 255) / 256), 256, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, heavy, counter + 1, col_grid);
     // every task is short (a heavy plane or a light column), so full occupancy.
     // 1. heavy planes; 2. the light columns on `s` while the latency-bound
     // in-order fix-up of the heavy columns runs beside them on a side stream
     const int64_t blocks = (int64_t)sm_count() * per_sm;
-    grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
-        grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
-        counter + 1, 0, col_grid);
+    if (spec2)
+        grid_newton_kernel<true><<<(unsigned)(sm_count() * per_sm2), NEWTON_THREADS, 0, s>>>(
+            grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter,
+            heavy, counter + 1, 0, col_grid, spec2_pos, spec2_code, cap);
+    else
+        grid_newton_kernel<false><<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
+            grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter,
+            heavy, counter + 1, 0, col_grid, nullptr, nullptr, 0);
     static cudaStream_t side = nullptr;
     static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     if (!side) {
@@ -865,12 +936,13 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     grid_newton_fixup_kernel<<<(unsigned)((n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS),
                                NEWTON_THREADS, 0, side>>>(grids, (int)n_grids, block_grid, *geom,
                                                           positions, valid, stats, heavy,
-                                                          counter + 1, col_grid);
+                                                          counter + 1, col_grid, spec2_pos,
+                                                          spec2_code, cap);
     cudaEventRecord(join_ev, side);
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);  // work counter for phase 1
-    grid_newton_kernel<<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
+    grid_newton_kernel<false><<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
-        counter + 1, 1, col_grid);
+        counter + 1, 1, col_grid, nullptr, nullptr, 0);
     cudaStreamWaitEvent(s, join_ev, 0);
     cudaFreeAsync(counter, s);
     return check_launch("grid_newton_kernel / grid_newton_fixup_kernel");
