@@ -116,9 +116,19 @@ struct __align__(16) MergeChild {
 };
 
 __global__ void merge_prep_kernel(const hhsar_grid_desc *__restrict__ d, int n, hhsar_geom g,
-                                  int kernel, MergeChild *__restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                                  int kernel, MergeChild *__restrict__ out,
+                                  const hhsar_grid_desc *__restrict__ parents, int n_parents,
+                                  int n_blocks, int32_t *__restrict__ block_parent) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) {
+        // then the parent of every merge block's first point (the merge
+        // kernel walks forward from it instead of a per-point search)
+        i -= n;
+        if (i < n_blocks)
+            block_parent[i] = find_by_offset(parents, n_parents,
+                                             parents[0].offset + (int64_t)i * MERGE_THREADS);
+        return;
+    }
     const hhsar_grid_desc &D = d[i];
     MergeChild c;
     const double inv_step = 1.0 / g.step;
@@ -298,15 +308,19 @@ merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, i
                    const double *__restrict__ positions, const uint8_t *__restrict__ valid,
                    const MergeChild *__restrict__ kids, int fanout,
                    const float2 *__restrict__ kv, hhsar_geom g, int downconvert,
-                   float2 *__restrict__ out, int64_t *__restrict__ flagged) {
+                   float2 *__restrict__ out, int64_t *__restrict__ flagged,
+                   const int32_t *__restrict__ block_parent) {
     const int64_t base = parents[0].offset;
     const int64_t i = base + (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
     if (i >= base + n_points) return;
+    // independent loads first: flag, position, the block's first parent
+    const uint8_t vi = valid[i];
+    const double x = positions[3 * i], y = positions[3 * i + 1], z = positions[3 * i + 2];
+    int p = block_parent[blockIdx.x];
     unsigned fl = 0;
-    if (valid[i]) {
-        const int p = find_by_offset(parents, n_parents, i);
+    if (vi) {
+        while (p + 1 < n_parents && parents[p + 1].offset <= i) ++p;
         const hhsar_grid_desc &P = parents[p];
-        const double x = positions[3 * i], y = positions[3 * i + 1], z = positions[3 * i + 2];
         const double phi_p =
             downconvert ? sdc_phase_fast(P.ext, box_gap_exact(P.ext), g.k_min, g.k_max, x, y, z)
                         : 0.0;
@@ -400,10 +414,18 @@ merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, do
 
 // Per-child constants for a merge launch (stream-ordered scratch).
 static int prep_children(const hhsar_grid_desc *kids, int64_t n, const hhsar_geom &g, int kernel,
-                         MergeChild **out, cudaStream_t s) {
-    if (cudaMallocAsync(out, n * sizeof(MergeChild), s) != cudaSuccess)
+                         MergeChild **out, cudaStream_t s,
+                         const hhsar_grid_desc *parents = nullptr, int n_parents = 0,
+                         int n_blocks = 0, int32_t **block_parent = nullptr) {
+    // one scratch block: the child records, then (merge levels) the table
+    if (cudaMallocAsync(out, n * sizeof(MergeChild) + (size_t)n_blocks * sizeof(int32_t), s) !=
+        cudaSuccess)
         return set_error(HHSAR_ECUDA, "merge: scratch allocation failed");
-    merge_prep_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(kids, (int)n, g, kernel, *out);
+    int32_t *bp = reinterpret_cast<int32_t *>(*out + n);
+    if (block_parent) *block_parent = bp;
+    const int64_t work = n + n_blocks;
+    merge_prep_kernel<<<(unsigned)((work + 127) / 128), 128, 0, s>>>(
+        kids, (int)n, g, kernel, *out, parents, n_parents, n_blocks, bp);
     return check_launch("merge_prep_kernel");
 }
 
@@ -494,16 +516,18 @@ extern "C" int hhsar_merge_level(const hhsar_grid_desc *parent_grids, int64_t n_
     auto kv = reinterpret_cast<const float2 *>(values_in);
     auto out = reinterpret_cast<float2 *>(values_out);
     MergeChild *kids = nullptr;
-    int rc = prep_children(child_grids, n_child_grids, *geom, kernel, &kids, s);
+    int32_t *block_parent = nullptr;
+    int rc = prep_children(child_grids, n_child_grids, *geom, kernel, &kids, s, parent_grids,
+                           (int)n_parents, (int)blocks, &block_parent);
     if (rc != HHSAR_OK) return rc;
     if (kernel == 0)
         merge_level_kernel<0><<<blocks, MERGE_THREADS, 0, s>>>(
             parent_grids, (int)n_parents, n_parent_points, positions, valid, kids, fanout,
-            kv, *geom, downconvert, out, flagged);
+            kv, *geom, downconvert, out, flagged, block_parent);
     else
         merge_level_kernel<1><<<blocks, MERGE_THREADS, 0, s>>>(
             parent_grids, (int)n_parents, n_parent_points, positions, valid, kids, fanout,
-            kv, *geom, downconvert, out, flagged);
+            kv, *geom, downconvert, out, flagged, block_parent);
     rc = check_launch("merge_level_kernel");
     cudaFreeAsync(kids, s);
     return rc;
