@@ -535,13 +535,16 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     if not gate:
         env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
         t0 = 0.0
-    with torch.cuda.stream(geo):
-        lat = finish_lattices(pending)
-    if gate:
-        b0, w = lat.gate
+    else:
+        # the plan's round trip, then the gated compression first: it fills
+        # the GPU while the host sizes the pools and launches Newton
+        pending["done"].synchronize()
+        b0, w = (int(v) for v in pending["host_s"][24:40].view(np.int64))
         if _trace:
             _trace("gate")
         env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
+    with torch.cuda.stream(geo):
+        lat = finish_lattices(pending)
     main.wait_stream(geo)
     # blocks allocated on the side stream are used on the main one from here
     for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
