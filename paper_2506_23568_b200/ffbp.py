@@ -472,6 +472,9 @@ def geometry_stream(device):
     return _GEO_STREAMS[key]
 
 
+NEWTON_FIRST_MAX_COLUMNS = 131072  # as the native NEWTON_SPEC2_MAX_COLS (grid.cu)
+
+
 def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
     """Delay-bin window [b0, b0 + w) that holds every delay the leaf stage can
     read.  A valid leaf point lies in its grid's slack box (ffbp.py:282-289,
@@ -536,15 +539,22 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
         t0 = 0.0
     else:
-        # the plan's round trip, then the gated compression first: it fills
-        # the GPU while the host sizes the pools and launches Newton
+        # after the plan's round trip: on large problems the gated
+        # compression goes first (it fills the GPU while the host sizes the
+        # pools and launches Newton); on small ones Newton's latency-bound
+        # fix-up is the critical path and goes first
         pending["done"].synchronize()
-        b0, w = (int(v) for v in pending["host_s"][24:40].view(np.int64))
+        n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
+        newton_first = n_cols <= NEWTON_FIRST_MAX_COLUMNS
+        if newton_first:
+            with torch.cuda.stream(geo):
+                lat = finish_lattices(pending)
         if _trace:
             _trace("gate")
         env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
-    with torch.cuda.stream(geo):
-        lat = finish_lattices(pending)
+    if not gate or not newton_first:
+        with torch.cuda.stream(geo):
+            lat = finish_lattices(pending)
     main.wait_stream(geo)
     # blocks allocated on the side stream are used on the main one from here
     for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
