@@ -512,12 +512,12 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
     high-priority side stream; once the plan's descriptors are on the host
     the range compression is launched on the caller's stream for the delay
-    bins the leaf stage can read only (leaf_range_gate; ``gate=False``
-    computes full profiles); the leaf stage waits for both.  The gate puts
-    the plan's host round trip ahead of the compression but shrinks the
-    profiles to the leaf stage's reach (config 2/3/4: 256/352/288 of
-    1,024/2,048/4,096 bins; config 4 68.7 GB of profiles -> 4.8 GB, RC
-    18.9 -> 14.6 ms; config 3 2.67 -> 2.57 ms per step).
+    bins the leaf stage can read only (hhsar_leaf_range_gate, computed with
+    the plan; ``gate=False`` computes full profiles); the leaf stage waits
+    for both.  The gate puts the plan's host round trip ahead of the
+    compression but shrinks the profiles to the leaf stage's reach (config
+    2/3/4: 256/352/288 of 1,024/2,048/4,096 bins; config 4 68.7 GB of
+    profiles -> 4.8 GB).
     """
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
@@ -535,6 +535,7 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi,
                                 gate_dt=dt if gate else None, gate_bins=n_t)
+    newton_first = False
     if not gate:
         env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
         t0 = 0.0
@@ -552,7 +553,7 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         if _trace:
             _trace("gate")
         env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
-    if not gate or not newton_first:
+    if not newton_first:
         with torch.cuda.stream(geo):
             lat = finish_lattices(pending)
     main.wait_stream(geo)
