@@ -230,6 +230,10 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
     rows = to_device_cube(np.asarray(cube.values)[e0:e1])
     vol, stats, flags, oow, sched, descs = hhffbpa_sharded_device(
         comm, rows, e0, el_dev, kgrid, region, dims, params, levels, merge_factor, upsample)
+    if int(oow.cpu()[0]):  # a leaf delay outside the range gate (all-reduced: every rank agrees)
+        vol, stats, flags, oow, sched, descs = hhffbpa_sharded_device(
+            comm, rows, e0, el_dev, kgrid, region, dims, params, levels, merge_factor, upsample,
+            gate=False)
     origin, step = region_grid(region, dims)
     extra = torch.cat([flags, stats.reshape(-1)])
     volume, tail = _finish(vol, oow, dims, origin, step, {}, extra)
@@ -243,12 +247,15 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
 
 
 def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, region, final_dims,
-                           params, levels: int, merge_factor: int, upsample: int):
+                           params, levels: int, merge_factor: int, upsample: int,
+                           gate: bool = True):
     """One rank's share of HHFFBPA:
 
     1. subaperture-group partition: the rank owns a contiguous run of
        subtrees up to the exchange level and range-compresses only those
-       elements (``cube_dev_rows`` = its rows, starting at ``e_row0``);
+       elements (``cube_dev_rows`` = its rows, starting at ``e_row0``), only
+       the delay bins the leaf stage can read (the plan's range gate, as in
+       ffbp.hhffbpa_from_cube; ``gate=False``: full profiles);
        every grid is PLANNED for the whole region on every rank (so lattices
        are identical to the 1-GPU ones), Newton runs only where this rank
        evaluates points;
@@ -261,9 +268,8 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     """
     import torch
     from .bpa import el_f32x4
-    from .ffbp import Pipeline
-    from .rangecomp import range_compress_device
-    env, dt, k_ref = range_compress_device(cube_dev_rows, kgrid, upsample)
+    from .ffbp import Pipeline, build_lattices, src_pad_of
+    from .rangecomp import profile_axis, range_compress_device, range_compress_window
     world, rank = comm.world, comm.rank
     sched, kx, owned, _ = plan_shard(el_dev.shape[0], levels, merge_factor, world, rank)
     n_lv = len(sched.level_slices)
@@ -271,9 +277,20 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     for k in range(n_lv):
         a, b = owned[k] if k <= kx else sched.level_slices[k]
         mask[a:b] = True
-    pipe = Pipeline(env, el_dev, el_f32x4(el_dev), 0.0, dt, k_ref, kgrid, region, final_dims,
-                    params, levels, merge_factor, newton_grids=mask, env_row0=e_row0,
-                    sched=sched)
+    n_t, dt, _, _ = profile_axis(kgrid, upsample)
+    window_hi = (n_t - 1) * dt
+    lat = build_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
+                         src_pad_of(params), window_hi, newton_grids=mask,
+                         gate_dt=dt if gate else None, gate_bins=n_t)
+    if gate:
+        b0, w = lat.gate
+        env, t0, dt, k_ref = range_compress_window(cube_dev_rows, kgrid, upsample, b0, w)
+    else:
+        env, dt, k_ref = range_compress_device(cube_dev_rows, kgrid, upsample)
+        t0 = 0.0
+    pipe = Pipeline(env, el_dev, el_f32x4(el_dev), t0, dt, k_ref, kgrid, region, final_dims,
+                    params, levels, merge_factor, window_hi, newton_grids=mask,
+                    env_row0=e_row0, sched=sched, lat=lat)
     pipe.leaves(*owned[0])
     for k in range(max(kx, 0)):
         pipe.merge(k, *owned[k + 1])

@@ -201,7 +201,7 @@ class Lattices:
 
 def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float,
                    pad: int, window_hi: float, tol: float = 1e-9, max_iter: int = 50,
-                   newton_grids=None) -> Lattices:
+                   newton_grids=None, gate_dt=None, gate_bins: int = 0) -> Lattices:
     """Plan + Newton for every grid of the schedule (ffbp.py:179-307).
 
     Every grid is planned (metadata is cheap and needed by any rank that
@@ -211,7 +211,7 @@ def build_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin:
     counters.
     """
     pending = plan_lattices(el_dev, sched, region, kgrid, gamma, margin, pad, window_hi, tol,
-                            max_iter)
+                            max_iter, gate_dt, gate_bins)
     return finish_lattices(pending, newton_grids)
 
 
