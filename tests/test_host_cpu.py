@@ -204,3 +204,33 @@ def test_profile_cut_matches_reference():
     cut, sp = metrics.profile_cut(ImageVolume(z["ref"], z["origin"], z["step"]), "y",
                                   (0.0, 0.0, 0.23))
     assert np.array_equal(cut, z["cut_y"]) and sp == float(z["cut_spacing"])
+
+
+def test_leaf_range_gate_host_restatement():
+    """ffbp.leaf_range_gate (the host restatement of hhsar_leaf_range_gate):
+    one leaf whose element box and slack box are unit-separated along z
+    gives the window of their nearest/farthest distances, widened by the
+    element-box diagonal and the 6-bin pad, rounded up to 32 bins and
+    clipped to the profile."""
+    from types import SimpleNamespace
+    descs = np.zeros(2, dtype=_native.GRID_DTYPE)
+    descs["box"][0] = [0.0, 0.0, 0.0, 0.01, 0.02, 0.0]       # elements: 1 x 2 cm at z = 0
+    descs["slack_lo"][0] = [-0.1, -0.1, 0.3]
+    descs["slack_hi"][0] = [0.1, 0.1, 0.4]
+    lat = SimpleNamespace(descs=descs)
+    sched = SimpleNamespace(level_slices=[(0, 1), (1, 2)])
+    c = model.C_LIGHT
+    dt = 2.0 * 0.005 / c                                    # 5 mm range bins
+    b0, w = ffbp.leaf_range_gate(lat, sched, dt, 4096)
+    inv_bin = 2.0 / (c * dt)
+    d_min = 0.3
+    far = np.maximum(np.abs(np.array([0.01, 0.02, 0.0]) - np.array([-0.1, -0.1, 0.3])),
+                     np.abs(np.array([0.1, 0.1, 0.4]) - np.array([0.0, 0.0, 0.0])))
+    d_max = float(np.sqrt((far ** 2).sum()))
+    margin = int(np.ceil(np.sqrt(0.01 ** 2 + 0.02 ** 2) * inv_bin)) + 6
+    want_b0 = int(np.floor(d_min * inv_bin)) - margin
+    want_b1 = int(np.ceil(d_max * inv_bin)) + margin + 1
+    assert b0 == want_b0 and w % 32 == 0 and b0 + w >= want_b1 and w - (want_b1 - want_b0) < 32
+    # clipped at the profile end
+    b0c, wc = ffbp.leaf_range_gate(lat, sched, dt, want_b1 - 5)
+    assert b0c == want_b0 and b0c + wc == want_b1 - 5
