@@ -303,7 +303,7 @@ __device__ __forceinline__ bool merge_point(const MergeChild *__restrict__ kids,
 }
 
 template <int KERNEL>
-__global__ void __launch_bounds__(MERGE_THREADS, KERNEL ? 1 : 12)
+__global__ void __launch_bounds__(MERGE_THREADS, KERNEL ? 8 : 12)
 merge_level_kernel(const hhsar_grid_desc *__restrict__ parents, int n_parents, int64_t n_points,
                    const double *__restrict__ positions, const uint8_t *__restrict__ valid,
                    const MergeChild *__restrict__ kids, int fanout,
