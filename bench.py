@@ -284,7 +284,7 @@ def run_ours(args):
             result["hhffbpa"] = {f"config{c}": hhffbpa_leg(c, dev, max(args.steps, 20))
                                  for c in (2, 3)}
             free, _ = torch.cuda.mem_get_info(dev)
-            if free > 120e9:  # config 4: 17 GB cube + 69 GB profiles + lattices
+            if free > 60e9:  # config 4: 17 GB cube + 4.8 GB gated profiles + lattices + volume
                 result["hhffbpa"]["config4"] = hhffbpa_leg(4, dev, min(args.steps, 3))
             result["hhffbpa"]["config2_leaf_sweep"] = leaf_sweep_leg(dev, args.steps)
             check = hhffbpa_leg(2, dev, 1, check=True)
