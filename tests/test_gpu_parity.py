@@ -326,7 +326,9 @@ def test_config3_full_scale_vs_oracle(hh):
 
 @pytest.mark.parametrize("n_el,n_f,upsample,b0,w", [(37, 256, 4, 80, 96), (9, 512, 4, 0, 64),
                                                     (5, 1024, 4, 4000, 96), (3, 128, 8, 300, 211),
-                                                    (4, 64, 4, 17, 239)])
+                                                    (4, 64, 4, 17, 239),
+                                                    (2000, 1024, 4, 49, 288),   # config 4 rows, its gate
+                                                    (3000, 512, 4, 0, 352)])    # config 3 rows, its gate
 def test_range_compress_window_equals_full_slice(n_el, n_f, upsample, b0, w):
     """The range-gated compression (only bins [b0, b0 + w) computed in the
     last pass and stored) against the same bins of the full compression."""
