@@ -6,8 +6,12 @@
  * stream handle (cudaStream_t passed as void*), and returns an int status:
  * 0 = OK, 1 = bad argument, 2 = CUDA error (hhsar_last_error() has text).
  * Calls are asynchronous on the given stream; nothing synchronises except
- * where noted.  No C++ exceptions cross the ABI and the library keeps no
- * global state besides the last-error string (thread-local).
+ * where noted.  No C++ exceptions cross the ABI.  Process-wide state: the
+ * last-error string (thread-local) and per-device caches -- SM count,
+ * kernel occupancy, one high-priority side stream per device (used by
+ * hhsar_grid_newton's fix-up) -- each created once under a mutex and keyed
+ * by the caller's current device, so calls are thread-safe per stream and
+ * one process may drive several GPUs.
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/hhsar):
  *   hhsar_bp_gather        <- _kernels.backproject_gather   (_kernels.py:98-110)
@@ -49,6 +53,10 @@ extern "C" {
 #define HHSAR_OK 0
 #define HHSAR_EINVAL 1
 #define HHSAR_ECUDA 2
+
+/* largest Newton iteration cap the batched grid build accepts (7-bit
+ * iteration counts; the reference default is 50, ffbp.py:182) */
+#define HHSAR_MAX_NEWTON_ITER 126
 
 /* Geometry constants shared by the grid, leaf and merge kernels.  Host code
  * computes every derived constant in float64 exactly as the reference does

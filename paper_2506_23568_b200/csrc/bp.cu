@@ -10,9 +10,6 @@ namespace hhsar {
 
 constexpr int BP_THREADS = 256;
 constexpr int BP_CHUNK = 512;   // elements staged per shared-memory pass
-constexpr int CART_V = 4;       // voxels per thread along x
-constexpr int CART_TZ = 64;     // tile: CART_V (x) x 4 (y) x 64 (z)
-constexpr int CART_TY = BP_THREADS / CART_TZ;
 
 struct BpConst {
     float inv_bin;   // 2 / (c * dt): metres -> delay-bin index
@@ -283,66 +280,6 @@ __global__ void add_parts_kernel(float2 *__restrict__ out, const float2 *__restr
     }
 }
 
-// Full-aperture BPA over region_grid voxels, flattened index in [vb, ve).
-// (First version, kept for A/B comparisons: HHSAR_BPA_KERNEL=simple.)
-__global__ void __launch_bounds__(BP_THREADS)
-bpa_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, double sz, int nx,
-                     int ny, int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el,
-                     int m, const float2 *__restrict__ env, BpConst k,
-                     float2 *__restrict__ out, int64_t *__restrict__ oow_total) {
-    __shared__ float4 s_el[BP_CHUNK];
-    // tile coordinates
-    const int tiles_z = (nz + CART_TZ - 1) / CART_TZ;
-    const int tiles_y = (ny + CART_TY - 1) / CART_TY;
-    const int tiles_x = (nx + CART_V - 1) / CART_V;
-    (void)tiles_x;
-    const int tile = blockIdx.x;
-    const int tz = tile % tiles_z, ty = (tile / tiles_z) % tiles_y, tx = tile / (tiles_z * tiles_y);
-    const int iz = tz * CART_TZ + (threadIdx.x % CART_TZ);
-    const int iy = ty * CART_TY + (threadIdx.x / CART_TZ);
-    const int ix0 = tx * CART_V;
-    // voxel coordinates exactly as numpy: origin + step * i (float64), then f32
-    const float py = (float)__dadd_rn(oy, __dmul_rn(sy, (double)iy));
-    const float pz = (float)__dadd_rn(oz, __dmul_rn(sz, (double)iz));
-    float px[CART_V];
-    bool live[CART_V];
-    int64_t flat[CART_V];
-#pragma unroll
-    for (int v = 0; v < CART_V; ++v) {
-        const int ix = ix0 + v;
-        px[v] = (float)__dadd_rn(ox, __dmul_rn(sx, (double)ix));
-        flat[v] = ((int64_t)ix * ny + iy) * nz + iz;
-        live[v] = ix < nx && iy < ny && iz < nz && flat[v] >= vb && flat[v] < ve;
-    }
-    float2 acc[CART_V];
-    unsigned bad = 0;
-#pragma unroll
-    for (int v = 0; v < CART_V; ++v) acc[v] = make_float2(0.f, 0.f);
-
-    for (int c0 = 0; c0 < m; c0 += BP_CHUNK) {
-        const int cn = min(BP_CHUNK, m - c0);
-        __syncthreads();
-        for (int j = threadIdx.x; j < cn; j += BP_THREADS) s_el[j] = el[c0 + j];
-        __syncthreads();
-        for (int j = 0; j < cn; ++j) {
-            const float4 e = s_el[j];
-            const float dy = py - e.y, dz = pz - e.z;
-            const float dyz = fmaf(dy, dy, dz * dz);
-            const float2 *row = env + (int64_t)(c0 + j) * k.n_t;
-#pragma unroll
-            for (int v = 0; v < CART_V; ++v) {
-                const float dx = px[v] - e.x;
-                const float d = sqrtf(fmaf(dx, dx, dyz));
-                if (live[v]) bad += !bp_unit(d, k, row, acc[v]);
-            }
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < CART_V; ++v)
-        if (live[v]) out[flat[v] - vb] = acc[v];
-    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
-}
-
 // Generic gather for arbitrary points (operator-level backproject_gather).
 __global__ void __launch_bounds__(BP_THREADS)
 bp_gather_kernel(const double *__restrict__ pts, int64_t n, const float4 *__restrict__ el, int m,
@@ -424,12 +361,7 @@ struct TileArgs {
 
 template <int VX, int MINB, bool PAIR>
 int launch_tile(const TileArgs &a) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpa_tile_kernel<VX, MINB, PAIR>,
-                                                      TL_THREADS, 0);
-        if (per_sm <= 0) per_sm = 1;
-    }
+    const int per_sm = occupancy((const void *)bpa_tile_kernel<VX, MINB, PAIR>, TL_THREADS);
     // only tiles intersecting [vb, ve) matter; x-slab sharding keeps that a
     // contiguous run of tile columns
     const int64_t plane = (int64_t)a.ny * a.nz;
@@ -484,11 +416,7 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
         cudaMemsetAsync(out, 0, (vox_end - vox_begin) * sizeof(float2), s);
         return check_launch("bpa_cartesian memset");
     }
-    static const bool simple = [] {
-        const char *v = getenv("HHSAR_BPA_KERNEL");
-        return v && v[0] == 's';
-    }();
-    if (!simple) {
+    {
         BpFast k;
         const BpConst c = make_bp_const(n_t, t0, dt, k_ref);
         k.inv_bin = c.inv_bin;
@@ -501,10 +429,6 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
         k.alpha_d = k_ref * HHSAR_C_LIGHT * dt;
         k.alpha = (float)k.alpha_d;
         k.kc_t0 = k_ref * HHSAR_C_LIGHT * t0;
-        static const int variant = [] {
-            const char *v = getenv("HHSAR_BPA_VARIANT");
-            return v ? atoi(v) : 0;
-        }();
         float2 *rot = nullptr;
         if (cudaMallocAsync(&rot, n_t * sizeof(float2), s) != cudaSuccess)
             return set_error(HHSAR_ECUDA, "bpa_cartesian: table allocation failed");
@@ -514,27 +438,12 @@ extern "C" int hhsar_bpa_cartesian(const double *origin, const double *step, con
                          reinterpret_cast<const float4 *>(el_xyz), (int)m,
                          reinterpret_cast<const float2 *>(envelopes), k,
                          reinterpret_cast<float2 *>(out), oow_total, rot, s};
-        int rc;
-        switch (variant) {
-            // A/B variants (HHSAR_BPA_VARIANT): VX voxels/thread, min CTAs/SM,
-            // packed fp32x2 pair path.  Default measured fastest on B200.
-            case 1: rc = launch_tile<4, 5, false>(a); break;
-            case 2: rc = launch_tile<8, 3, false>(a); break;
-            case 3: rc = launch_tile<8, 3, true>(a); break;
-            case 4: rc = launch_tile<4, 4, true>(a); break;
-            default: rc = launch_tile<4, 5, true>(a); break;
-        }
+        // 4 voxels per thread, 5 CTAs/SM, packed fp32x2 voxel pairs
+        // (measured fastest of the VX / CTAs-per-SM / pair variants on B200)
+        const int rc = launch_tile<4, 5, true>(a);
         cudaFreeAsync(rot, s);
         return rc;
     }
-    const int64_t tiles = (int64_t)((nx + CART_V - 1) / CART_V) * ((ny + CART_TY - 1) / CART_TY) *
-                          ((nz + CART_TZ - 1) / CART_TZ);
-    bpa_cartesian_kernel<<<(unsigned)tiles, BP_THREADS, 0, s>>>(
-        origin[0], origin[1], origin[2], step[0], step[1], step[2], nx, ny, nz, vox_begin,
-        vox_end, reinterpret_cast<const float4 *>(el_xyz), (int)m,
-        reinterpret_cast<const float2 *>(envelopes), make_bp_const(n_t, t0, dt, k_ref),
-        reinterpret_cast<float2 *>(out), oow_total);
-    return check_launch("bpa_cartesian_kernel");
 }
 
 extern "C" int hhsar_bp_gather(const double *points, int64_t n, const double *el_pos, int64_t m,

@@ -19,7 +19,14 @@ int check_launch(const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-int sm_count();
+int sm_count();                  // SM count of the current device (cached per device)
+int current_device();
+// Resident CTAs per SM of `kernel` at `threads` threads (cached per device
+// and kernel, thread-safe).
+int occupancy(const void *kernel, int threads, size_t smem = 0);
+// High-priority non-blocking stream of the current device (created once,
+// thread-safe); nullptr if it cannot be created.
+cudaStream_t side_stream();
 
 // ---- exact float64 arithmetic ----------------------------------------------
 // numpy evaluates each ufunc separately with IEEE round-to-nearest and never

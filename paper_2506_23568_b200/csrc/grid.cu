@@ -462,7 +462,7 @@ __device__ __forceinline__ void flush_stats(int64_t *__restrict__ stats, int gi,
 // counts are unchanged; all tasks are short, so the persistent kernel can
 // run at full occupancy without a long tail.
 __device__ __forceinline__ uint8_t spec_code(bool ok, int it) {
-    return (uint8_t)((ok ? 0x80 : 0) | (it & 0x7f));  // it <= max_iter <= 127
+    return (uint8_t)((ok ? 0x80 : 0) | (it & 0x7f));  // it <= max_iter <= 126 (checked at entry)
 }
 
 __global__ void grid_newton_heavy_list_kernel(const hhsar_grid_desc *__restrict__ grids,
@@ -857,6 +857,8 @@ extern "C" int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const do
     HHSAR_REQUIRE(n_grids > 0 && n_grids < (1ll << 31), "grid_plan: bad grid count");
     HHSAR_REQUIRE(n_b > 0 && geom != nullptr, "grid_plan: bad boundary lattice");
     HHSAR_REQUIRE(geom->step > 0.0 && geom->step <= 1.0, "grid_plan: step must lie in (0, 1]");
+    HHSAR_REQUIRE(geom->max_iter >= 1 && geom->max_iter <= HHSAR_MAX_NEWTON_ITER,
+                  "grid_plan: max_iter must lie in [1, 126]");
     grid_plan_kernel<<<(unsigned)n_grids, PLAN_THREADS, 0, as_stream(stream)>>>(
         grids, leaf_box, boundary, (int)n_b, *geom, status);
     if (totals != nullptr) {
@@ -874,26 +876,19 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
                                  double *positions, uint8_t *valid, int64_t *stats,
                                  void *stream) {
     HHSAR_REQUIRE(n_grids > 0 && n_cols >= 0 && geom != nullptr, "grid_newton: bad sizes");
+    // iteration counts travel in 7 bits next to the ok flag (spec_code), and
+    // 0xff (ok at 127 iterations) is the "no continuation" sentinel
+    HHSAR_REQUIRE(geom->max_iter >= 1 && geom->max_iter <= HHSAR_MAX_NEWTON_ITER,
+                  "grid_newton: max_iter must lie in [1, 126]");
     if (n_cols == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
-    static int per_sm = 0, per_sm2 = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_newton_kernel<false>,
-                                                      NEWTON_THREADS, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, grid_newton_kernel<true>,
-                                                      NEWTON_THREADS, 0);
-        if (per_sm <= 0) per_sm = 1;
-        if (per_sm2 <= 0) per_sm2 = 1;
-    }
+    const int per_sm = occupancy((const void *)grid_newton_kernel<false>, NEWTON_THREADS);
+    const int per_sm2 = occupancy((const void *)grid_newton_kernel<true>, NEWTON_THREADS);
     // Speculative warm continuations of the heavy planes (SPEC2) pay where
     // the in-order fix-up is the critical path, i.e. small problems (config
     // 2: 39 k columns); on large ones the heavy phase is throughput work
     // competing with the range compression, and they are off.
-    static const int spec2_env = [] {
-        const char *e = getenv("HHSAR_NEWTON_SPEC2");
-        return e ? atoi(e) : -1;
-    }();
-    const bool spec2 = spec2_env >= 0 ? spec2_env != 0 : n_cols <= NEWTON_SPEC2_MAX_COLS;
+    const bool spec2 = n_cols <= NEWTON_SPEC2_MAX_COLS;
     const int64_t cap = spec2 ? (n_cols / 8 > 256 ? n_cols / 8 : 256) : 0;  // heavy columns with slots
     // scratch: [0] work counter, [1] heavy-column count, then the heavy list,
     // the column -> grid map, and (SPEC2) the continuation slots
@@ -922,28 +917,35 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
         grid_newton_kernel<false><<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
             grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter,
             heavy, counter + 1, 0, col_grid, nullptr, nullptr, 0);
-    static cudaStream_t side = nullptr;
-    static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    if (!side) {
-        int lo = 0, hi = 0;  // the fix-up must not queue behind range-compression CTAs
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
-        cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+    // the fix-up runs on the device's high-priority side stream (it must not
+    // queue behind range-compression CTAs); fork/join events are per call
+    cudaStream_t side = side_stream();
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    if (side == nullptr || cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming) != cudaSuccess) {
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        side = s;  // no side stream: run the fix-up in order on the caller's stream
+        fork_ev = join_ev = nullptr;
     }
-    cudaEventRecord(fork_ev, s);
-    cudaStreamWaitEvent(side, fork_ev, 0);
+    if (fork_ev) {
+        cudaEventRecord(fork_ev, s);
+        cudaStreamWaitEvent(side, fork_ev, 0);
+    }
     grid_newton_fixup_kernel<<<(unsigned)((n_cols + NEWTON_THREADS - 1) / NEWTON_THREADS),
                                NEWTON_THREADS, 0, side>>>(grids, (int)n_grids, block_grid, *geom,
                                                           positions, valid, stats, heavy,
                                                           counter + 1, col_grid, spec2_pos,
                                                           spec2_code, cap);
-    cudaEventRecord(join_ev, side);
+    if (join_ev) cudaEventRecord(join_ev, side);
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);  // work counter for phase 1
     grid_newton_kernel<false><<<(unsigned)blocks, NEWTON_THREADS, 0, s>>>(
         grids, (int)n_grids, n_cols, block_grid, *geom, positions, valid, stats, counter, heavy,
         counter + 1, 1, col_grid, nullptr, nullptr, 0);
-    cudaStreamWaitEvent(s, join_ev, 0);
+    if (join_ev) {
+        cudaStreamWaitEvent(s, join_ev, 0);
+        cudaEventDestroy(fork_ev);  // released once the recorded work completes
+        cudaEventDestroy(join_ev);
+    }
     cudaFreeAsync(counter, s);
     return check_launch("grid_newton_kernel / grid_newton_fixup_kernel");
 }

@@ -59,8 +59,6 @@ compact_leaf_kernel(const hhsar_grid_desc *__restrict__ grids, const uint8_t *__
     if (threadIdx.x == 0) cnt[blockIdx.x] = running;
 }
 
-__device__ unsigned long long g_leaf_checked;  // (CTA, element) pairs on the checked path
-__device__ unsigned long long g_leaf_tw[4];    // CTAs per window width 32 / 64 / 128 / 256
 
 // Carrier rotation per delay bin, exp(j k_ref c (t0 + dt bin)), float64 phase
 // reduced then rounded once: shared by every element's window staging.
@@ -152,7 +150,6 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __syncthreads();
     for (int w = 0; w < LP_THREADS / 32; ++w) need = max(need, __float_as_int(s_box[0][w]));
     const int lw = need <= 32 ? 5 : need <= 64 ? 6 : need <= 128 ? 7 : 8;  // log2 TW
-    if (t == 0) atomicAdd(&g_leaf_tw[lw - 5], 1ull);
     const int TW = 1 << lw, LP_CHUNK = WIN >> lw;
     f2x pa[P], pb[P];
 #pragma unroll
@@ -226,7 +223,6 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         };
         // checked path: exact reference skip-and-count, global gathers
         auto checked_unit = [&](const float4 &e, int j) {
-            if (t == 0) atomicAdd(&g_leaf_checked, 1ull);
             const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
 #pragma unroll
             for (int q = 0; q < P; ++q) {
@@ -319,20 +315,3 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
 }
 
 }  // namespace hhsar
-
-// Diagnostics (not part of the product ABI): number of (CTA, element) pairs
-// that took the checked global-gather path since the last call.
-extern "C" unsigned long long hhsar_debug_leaf_checked(void) {
-    unsigned long long v = 0, z = 0;
-    cudaMemcpyFromSymbol(&v, hhsar::g_leaf_checked, sizeof(v));
-    cudaMemcpyToSymbol(hhsar::g_leaf_checked, &z, sizeof(z));
-    return v;
-}
-
-// Diagnostics: CTAs per staged window width (32, 64, 128, 256 bins) since
-// the last call, into out[4].
-extern "C" void hhsar_debug_leaf_tw(unsigned long long *out) {
-    unsigned long long z[4] = {0, 0, 0, 0};
-    cudaMemcpyFromSymbol(out, hhsar::g_leaf_tw, sizeof(z));
-    cudaMemcpyToSymbol(hhsar::g_leaf_tw, z, sizeof(z));
-}

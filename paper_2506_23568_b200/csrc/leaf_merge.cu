@@ -1,11 +1,10 @@
 // Level-1 subimages and the merge stages (reference: ffbp.py:310-412 and
 // ffbp.py:493-495; interpolation _kernels.py:117-200).
 //
-// Leaf BPA: one CTA per (leaf grid, slice); the leaf's elements are staged in
-// shared memory and every valid lattice point sums them (same unit as the
-// direct BPA), then the epilogue applies the leaf's spatial downconversion
-// exp(-j Phi(pos)) (ffbp.py:343-348) so the stored lattice is ready to be
-// interpolated by the next level.
+// Leaf BPA (hhsar_leaf_bp): the C-ABI entry point; the kernel lives in
+// leaf2.cu (leaf_points_kernel: compacted valid points, delay windows staged
+// in shared memory, downconversion exp(-j Phi(pos)) (ffbp.py:343-348) fused
+// into the store so the lattice is ready for the next level).
 //
 // Merge: one thread per parent lattice point (or Cartesian voxel).  For every
 // child: compressed coordinates (float64), lattice interpolation of the
@@ -16,14 +15,7 @@
 
 namespace hhsar {
 
-constexpr int LEAF_THREADS = 256;
-constexpr int LEAF_CHUNK = 512;
 constexpr int MERGE_THREADS = 128;
-
-struct LeafConst {
-    float inv_bin, x0, rev, xmax;
-    int n_t;
-};
 
 __device__ __forceinline__ int find_by_offset(const hhsar_grid_desc *__restrict__ grids, int n,
                                               int64_t key) {
@@ -33,70 +25,6 @@ __device__ __forceinline__ int find_by_offset(const hhsar_grid_desc *__restrict_
         if (grids[mid].offset <= key) lo = mid; else hi = mid - 1;
     }
     return lo;
-}
-
-__global__ void __launch_bounds__(LEAF_THREADS)
-leaf_bp_kernel(const hhsar_grid_desc *__restrict__ grids, int slices,
-               const double *__restrict__ positions, const uint8_t *__restrict__ valid,
-               const float4 *__restrict__ el, const float2 *__restrict__ env, LeafConst k,
-               hhsar_geom g, int downconvert, float2 *__restrict__ values,
-               int64_t *__restrict__ oow_total) {
-    __shared__ float4 s_el[LEAF_CHUNK];
-    const hhsar_grid_desc &D = grids[blockIdx.x / slices];
-    const int slice = blockIdx.x % slices;
-    const int64_t npts = (int64_t)D.dims[0] * D.dims[1] * D.dims[2];
-    const int64_t e0 = D.start, m = D.stop - D.start;
-    const double gap = box_gap_exact(D.ext);
-    unsigned bad = 0;
-    for (int64_t base = (int64_t)slice * LEAF_THREADS; base < npts;
-         base += (int64_t)slices * LEAF_THREADS) {
-        const int64_t i = base + threadIdx.x;
-        const bool live = i < npts && valid[D.offset + i];
-        double px = 0, py = 0, pz = 0;
-        if (live) {
-            px = positions[3 * (D.offset + i)];
-            py = positions[3 * (D.offset + i) + 1];
-            pz = positions[3 * (D.offset + i) + 2];
-        }
-        const float fx = (float)px, fy = (float)py, fz = (float)pz;
-        float2 acc = make_float2(0.f, 0.f);
-        for (int64_t c0 = 0; c0 < m; c0 += LEAF_CHUNK) {
-            const int cn = (int)min((int64_t)LEAF_CHUNK, m - c0);
-            __syncthreads();
-            for (int j = threadIdx.x; j < cn; j += LEAF_THREADS) s_el[j] = el[e0 + c0 + j];
-            __syncthreads();
-            if (live)
-                for (int j = 0; j < cn; ++j) {
-                    const float4 e = s_el[j];
-                    const float dx = fx - e.x, dy = fy - e.y, dz = fz - e.z;
-                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    const float x = fmaf(d, k.inv_bin, -k.x0);
-                    if (!(x >= 0.f && x <= k.xmax)) { ++bad; continue; }
-                    const int ib = min((int)x, k.n_t - 2);
-                    const float f = x - (float)ib;
-                    const float2 *row = env + (e0 + c0 + j) * (int64_t)k.n_t;
-                    const float2 v0 = __ldg(row + ib), v1 = __ldg(row + ib + 1);
-                    const float er = fmaf(f, v1.x - v0.x, v0.x), ei = fmaf(f, v1.y - v0.y, v0.y);
-                    const float rv = d * k.rev;
-                    float s, cc;
-                    __sincosf(6.283185307f * __fsub_rn(rv, rintf(rv)), &s, &cc);
-                    acc.x = fmaf(er, cc, fmaf(-ei, s, acc.x));
-                    acc.y = fmaf(er, s, fmaf(ei, cc, acc.y));
-                }
-        }
-        if (i < npts) {
-            float2 outv = make_float2(0.f, 0.f);
-            if (live) {
-                outv = acc;
-                if (downconvert) {
-                    const double phi = sdc_phase_fast(D.ext, gap, g.k_min, g.k_max, px, py, pz);
-                    outv = cmul(acc, cis_reduced(-phi));
-                }
-            }
-            values[D.offset + i] = outv;
-        }
-    }
-    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
 }
 
 // ---- merge stages -----------------------------------------------------------
@@ -474,31 +402,11 @@ extern "C" int hhsar_leaf_bp(const hhsar_grid_desc *grids, int64_t n_grids, int6
     HHSAR_REQUIRE(n_t >= 2, "leaf_bp: n_t must be >= 2");
     HHSAR_REQUIRE(point_begin >= 0 && point_end >= point_begin && point_end < (1ll << 31) &&
                   max_grid_points >= 0, "leaf_bp: bad point range");
-    static const bool simple = [] {
-        const char *v = getenv("HHSAR_LEAF_KERNEL");
-        return v && v[0] == 's';
-    }();
-    if (!simple)
-        return launch_leaf_points(grids, n_grids, max_grid_points, point_begin, point_end,
-                                  positions, valid, reinterpret_cast<const float4 *>(el_xyz),
-                                  reinterpret_cast<const float2 *>(envelopes), n_t, t0, dt, k_ref,
-                                  *geom, downconvert, reinterpret_cast<float2 *>(values),
-                                  oow_total, as_stream(stream));
-    LeafConst k;
-    k.inv_bin = (float)(2.0 / (HHSAR_C_LIGHT * dt));
-    k.x0 = (float)(t0 / dt);
-    k.rev = (float)(k_ref / 3.141592653589793);
-    k.xmax = (float)(n_t - 1);
-    k.n_t = (int)n_t;
-    // enough CTAs for two waves of the SMs
-    int slices = (int)((2 * sm_count() + n_grids - 1) / n_grids);
-    if (slices < 1) slices = 1;
-    if (slices > 64) slices = 64;
-    leaf_bp_kernel<<<(unsigned)(n_grids * slices), LEAF_THREADS, 0, as_stream(stream)>>>(
-        grids, slices, positions, valid, reinterpret_cast<const float4 *>(el_xyz),
-        reinterpret_cast<const float2 *>(envelopes), k, *geom, downconvert,
-        reinterpret_cast<float2 *>(values), oow_total);
-    return check_launch("leaf_bp_kernel");
+    return launch_leaf_points(grids, n_grids, max_grid_points, point_begin, point_end, positions,
+                              valid, reinterpret_cast<const float4 *>(el_xyz),
+                              reinterpret_cast<const float2 *>(envelopes), n_t, t0, dt, k_ref,
+                              *geom, downconvert, reinterpret_cast<float2 *>(values), oow_total,
+                              as_stream(stream));
 }
 
 extern "C" int hhsar_merge_level(const hhsar_grid_desc *parent_grids, int64_t n_parents,

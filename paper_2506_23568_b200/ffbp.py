@@ -42,6 +42,7 @@ from .rangecomp import RangeProfileSet, profile_axis, range_compress, to_device_
 from .spectrum import TWO_PI, SubarrayExtents
 
 GRID_PAD = 2  # ffbp.py:32
+MAX_NEWTON_ITER = 126  # HHSAR_MAX_NEWTON_ITER (include/hhsar_b200.h)
 BOUNDARY_PER_AXIS = 5  # ffbp.py:237
 
 
@@ -788,6 +789,9 @@ def build_subimage_grid(aperture, subarray, region, kgrid, gamma: float = 1.4,
         raise ConfigError("region must sit strictly in front of the array")
     if int(pad) != pad or pad < 1:
         raise ConfigError("pad must be an integer >= 1")
+    if not 1 <= int(max_iter) <= MAX_NEWTON_ITER:
+        # the batched grid build carries iteration counts in 7 bits
+        raise ConfigError(f"max_iter must lie in [1, {MAX_NEWTON_ITER}]")
     _native.library()
     el_dev = torch.as_tensor(np.ascontiguousarray(el), device="cuda")
     sched = Schedule(el.shape[0], 1)

@@ -3,9 +3,13 @@
 Mirrors rangecomp.range_compress (/root/reference/pkg/src/hhsar/rangecomp.py:
 61-101): an unnormalised zero-padded inverse DFT over the n_f frequency
 samples to n_t = upsample * n_f delay bins, then demodulation from the band
-start to the band-centre carrier k_ref.  The IDFT is a batched cuFFT (through
-torch.fft, norm="forward" = no 1/n factor); the demodulation is the
-hhsar_range_demod kernel (float64 phase per bin).  The result stays in HBM
+start to the band-centre carrier k_ref.  For power-of-two n_t in [16, 8192]
+(every BASELINE config) this is one fused kernel (hhsar_range_compress:
+pad + radix-16 Stockham IDFT + demodulation in a single HBM pass, or
+hhsar_range_compress_window for a delay-bin window); other n_t, or
+HHSAR_RANGE_FFT=cufft, use a batched cuFFT through torch.fft (norm="forward"
+= no 1/n factor) followed by the hhsar_range_demod kernel (float64 phase per
+bin).  The result stays in HBM
 as envelopes[N_el][n_t] complex64, time fastest -- the layout every
 backprojection kernel reads.
 """

@@ -1,5 +1,5 @@
-"""Median device time of the config-1 BPA kernel call (hhsar_bpa_cartesian),
-for A/B-ing kernel variants (HHSAR_BPA_VARIANT) in separate processes."""
+"""Median device time of the config-1 BPA kernel call (hhsar_bpa_cartesian);
+HHSAR_LIB=<other build> A/Bs another library build in a separate process."""
 import os
 import statistics
 import sys
@@ -29,9 +29,9 @@ def main():
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e))
     ms = statistics.median(times[1:])
-    print(f"variant {os.environ.get('HHSAR_BPA_VARIANT', '0')}: {ms:.3f} ms, "
+    print(f"lib {os.environ.get('HHSAR_LIB', 'default')}: {ms:.3f} ms, "
           f"{w.bpa_units / ms / 1e6:.1f} Gunit/s")
-    np.save(f"/tmp/bpa_out_{os.environ.get('HHSAR_BPA_VARIANT', '0')}.npy", out.cpu().numpy())
+    np.save(f"/tmp/bpa_out_{Path(os.environ.get('HHSAR_LIB', 'default')).stem}.npy", out.cpu().numpy())
 
 
 if __name__ == "__main__":
