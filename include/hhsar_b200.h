@@ -39,7 +39,8 @@
  *                             parent of a level (ffbp.py:351-412)
  *   hhsar_merge_cartesian  <- the final Cartesian landing (ffbp.py:493-495)
  *   hhsar_downconvert      <- ffbp._downconvert_samples (ffbp.py:343-348)
- *   hhsar_simulate         <- simulator.simulate_measurement (simulator.py:41-69)
+ *   hhsar_simulate / hhsar_simulate_uniform
+ *                          <- simulator.simulate_measurement (simulator.py:41-69)
  */
 #ifndef HHSAR_B200_H
 #define HHSAR_B200_H
@@ -278,6 +279,14 @@ int hhsar_merge_cartesian(const double *origin, const double *step, const int64_
 int hhsar_simulate(const double *el_pos, int64_t n_el, const double *pos,
                    const double *refl, int64_t n_s, const double *k, int64_t n_f,
                    void *out, void *stream);
+
+/* The same Born cube on a uniform frequency grid k_f = k0 + f dk (every
+ * FrequencyGrid, model.py:30-70): float64 distance and phase seed per 8
+ * frequencies, fp32 phasor recurrence and accumulation (~1e-5 relative to
+ * hhsar_simulate; the input generator for the large configs).  n_f <= 2048. */
+int hhsar_simulate_uniform(const double *el_pos, int64_t n_el, const double *pos,
+                           const double *refl, int64_t n_s, double k0, double dk, int64_t n_f,
+                           void *out, void *stream);
 
 /* ---- image-quality metrics ------------------------------ */
 

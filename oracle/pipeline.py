@@ -28,6 +28,7 @@ __all__ = [
     "llt_forward", "invert_newton", "interpolate", "build_grid", "level1",
     "merge_onto_points", "merge_children", "hhffbpa_reconstruct",
     "default_grid_dims", "leaf_bounds", "tree_levels", "threads", "simulate",
+    "Plan", "plan_grid", "grid_levels",
 ]
 
 C_LIGHT = 299792458.0
@@ -367,18 +368,24 @@ def _check_core(g: Grid):
                                 "no valid inverse position")
 
 
-def build_grid(ext, region, k_min, k_max, gamma=1.4, margin=0.25, tol=1e-9,
-               max_iter=50, pad=GRID_PAD, start=0, stop=0, prune=False) -> Grid:
-    """build_subimage_grid (ffbp.py:179-307) for a lateral extents box.
+@dataclass
+class Plan:
+    """Lattice metadata of build_subimage_grid before Newton (ffbp.py:237-304)."""
+    origin: np.ndarray
+    step: np.ndarray
+    counts: np.ndarray
+    lo: np.ndarray
+    hi: np.ndarray
+    axes: list
+    near: list
+    core: tuple
 
-    ``prune`` skips Newton on (u, v) columns outside the near band, whose
-    points end up masked whatever Newton returns (SURVEY G3); masks and
-    valid positions are unchanged, masked positions are left as guesses.
-    """
-    if not gamma >= 1.0:
-        raise OracleConfigError("oversampling factor must be at least 1")
-    if region.z_min <= 0.0:
-        raise OracleConfigError("region must sit strictly in front of the array")
+
+def plan_grid(ext, region, k_min, k_max, gamma=1.4, pad=GRID_PAD) -> Plan:
+    """The data-independent part of build_subimage_grid: bounds from
+    llt_forward on the region's 5^3 boundary lattice (ffbp.py:237-243),
+    u/v plane trimming (ffbp.py:248-257), near band (ffbp.py:294-301) and
+    core box (ffbp.py:302-304)."""
     b = _bounds(region)
     axes5 = [np.linspace(lo, hi, 5) for lo, hi in b]
     mesh = np.meshgrid(*axes5, indexing="ij")
@@ -396,11 +403,6 @@ def build_grid(ext, region, k_min, k_max, gamma=1.4, margin=0.25, tol=1e-9,
             origin[a] += first * step[a]
             counts[a] = last - first + 1
     axes = [origin[a] + step[a] * np.arange(counts[a]) for a in range(3)]
-    center = np.array([(b[a, 0] + b[a, 1]) / 2 for a in range(3)])
-    extent = b[:, 1] - b[:, 0]
-    max_step = 0.5 * float(np.linalg.norm(extent))
-    slack = margin * extent + 3.0 * GRID_PAD * step * extent / np.maximum(hi - lo, 1e-12)
-    nu, nv, nn = (int(c) for c in counts)
     eps = 1e-9 * step
     near = [(axes[a] >= lo[a] - GRID_PAD * step[a] - eps[a])
             & (axes[a] <= hi[a] + GRID_PAD * step[a] + eps[a]) for a in range(3)]
@@ -408,6 +410,31 @@ def build_grid(ext, region, k_min, k_max, gamma=1.4, margin=0.25, tol=1e-9,
     for a in range(3):
         img = (axes[a] >= lo[a] - eps[a]) & (axes[a] <= hi[a] + eps[a])
         core.append((int(np.argmax(img)), int(counts[a] - 1 - np.argmax(img[::-1]))))
+    return Plan(origin=origin, step=step, counts=counts, lo=lo, hi=hi, axes=axes, near=near,
+                core=tuple(core))
+
+
+def build_grid(ext, region, k_min, k_max, gamma=1.4, margin=0.25, tol=1e-9,
+               max_iter=50, pad=GRID_PAD, start=0, stop=0, prune=False) -> Grid:
+    """build_subimage_grid (ffbp.py:179-307) for a lateral extents box.
+
+    ``prune`` skips Newton on (u, v) columns outside the near band, whose
+    points end up masked whatever Newton returns (SURVEY G3); masks and
+    valid positions are unchanged, masked positions are left as guesses.
+    """
+    if not gamma >= 1.0:
+        raise OracleConfigError("oversampling factor must be at least 1")
+    if region.z_min <= 0.0:
+        raise OracleConfigError("region must sit strictly in front of the array")
+    b = _bounds(region)
+    pl = plan_grid(ext, region, k_min, k_max, gamma, pad)
+    origin, step, counts, lo, hi = pl.origin, pl.step, pl.counts, pl.lo, pl.hi
+    axes, near, core = pl.axes, pl.near, pl.core
+    center = np.array([(b[a, 0] + b[a, 1]) / 2 for a in range(3)])
+    extent = b[:, 1] - b[:, 0]
+    max_step = 0.5 * float(np.linalg.norm(extent))
+    slack = margin * extent + 3.0 * GRID_PAD * step * extent / np.maximum(hi - lo, 1e-12)
+    nu, nv, nn = (int(c) for c in counts)
 
     uu, vv = np.meshgrid(axes[0], axes[1], indexing="ij")
     uu, vv = uu.ravel(), vv.ravel()

@@ -74,6 +74,7 @@ SIGNATURES = {
     "hhsar_merge_cartesian": ([_P, _P, _P, _I64, _I64, _P, _I64, _P, _P, _I32, _P, _P, _P],
                               ctypes.c_int),
     "hhsar_simulate": ([_P, _I64, _P, _P, _I64, _P, _I64, _P, _P], ctypes.c_int),
+    "hhsar_simulate_uniform": ([_P, _I64, _P, _P, _I64, _D, _D, _I64, _P, _P], ctypes.c_int),
 }
 
 _lib = None
@@ -183,6 +184,30 @@ def simulate(elements, positions, refl, k_samples, device="cuda"):
     out = torch.empty((el.shape[0], k.shape[0]), dtype=torch.complex64, device=device)
     call("hhsar_simulate", ptr(el), el.shape[0], ptr(pos), ptr(rr), pos.shape[0],
          ptr(k), k.shape[0], ptr(out), stream_handle())
+    return out
+
+
+def simulate_uniform(elements, positions, refl, freqs, device="cuda", out=None):
+    """Born cube on the device for a uniform FrequencyGrid
+    (hhsar_simulate_uniform: fp32 phasor recurrence, float64 seeds) --
+    the generator for the large configs; complex64 tensor [N_el, n_f]
+    (written into ``out`` when given, e.g. a row slice of a bigger cube)."""
+    import torch
+    library()
+    if isinstance(elements, torch.Tensor):
+        el = elements.to(device=device, dtype=torch.float64).contiguous()
+    else:
+        el = torch.as_tensor(np.ascontiguousarray(elements, dtype=np.float64), device=device)
+    pos = torch.tensor(np.asarray(positions, dtype=np.float64).reshape(-1, 3), device=device)
+    r = np.ascontiguousarray(np.asarray(refl, dtype=np.complex128))
+    rr = torch.as_tensor(r.view(np.float64), device=device)
+    n_f = int(freqs.count)
+    k0 = float(freqs.k_min)
+    dk = (float(freqs.k_max) - k0) / (n_f - 1) if n_f > 1 else 0.0
+    if out is None:
+        out = torch.empty((el.shape[0], n_f), dtype=torch.complex64, device=device)
+    call("hhsar_simulate_uniform", ptr(el), el.shape[0], ptr(pos), ptr(rr), pos.shape[0], k0,
+         dk, n_f, ptr(out), stream_handle())
     return out
 
 

@@ -382,6 +382,78 @@ simulate_kernel(const double *__restrict__ el, const double *__restrict__ pos,
     }
 }
 
+
+// Born cube on a uniform frequency grid k_f = k0 + f dk (FrequencyGrid is
+// uniform by construction, model.py:30-70): exp(-2j k_f d) for the SIM_G
+// consecutive frequencies of a thread is a float64-seeded fp32 phasor times
+// powers of the per-scatterer step exp(-2j dk d).  One fp64 seed and one
+// MUFU sincos per SIM_G terms, the rest are fp32 complex FMAs: ~10x the
+// throughput of simulate_kernel (config 4's 4.3e13 terms in seconds instead
+// of minutes).  Accuracy: the recurrence adds ~SIM_G ulp of phase, the fp32
+// sum ~sqrt(n_s) ulp -- far below the complex64 quantisation the cube gets
+// anyway; both reconstruction paths read the same cube, so parity does not
+// depend on it.
+constexpr int SIM_G = 8;         // frequencies per thread
+constexpr int SIM_UTHREADS = 256;
+constexpr int SIM_SLOTS = 512;   // staged (element, scatterer) pairs per CTA pass
+
+__global__ void __launch_bounds__(SIM_UTHREADS)
+simulate_uniform_kernel(const double *__restrict__ el, int64_t n_el,
+                        const double *__restrict__ pos, const double *__restrict__ refl, int n_s,
+                        double k0, double dk, int n_f, float2 *__restrict__ out) {
+    __shared__ double s_d[SIM_SLOTS];      // -2 d per (element, scatterer)
+    __shared__ float2 s_step[SIM_SLOTS];   // exp(-2j dk d)
+    __shared__ float2 s_r[SIM_SLOTS];      // reflectivity per scatterer
+    const int per_el = (n_f + SIM_G - 1) / SIM_G;   // threads per element
+    const int els = SIM_UTHREADS / per_el;          // elements per CTA (>= 1)
+    const int ch = SIM_SLOTS / els;                 // scatterers per pass
+    const int t = threadIdx.x;
+    const int le = t / per_el, fg = t % per_el;
+    const int64_t e0 = (int64_t)blockIdx.x * els;
+    const int64_t e = e0 + le;
+    const bool live = le < els && e < n_el;
+    const int f0 = fg * SIM_G;
+    const double kf0 = k0 + dk * (double)f0;
+    float2 acc[SIM_G];
+#pragma unroll
+    for (int i = 0; i < SIM_G; ++i) acc[i] = make_float2(0.f, 0.f);
+    for (int s0 = 0; s0 < n_s; s0 += ch) {
+        const int sn = min(ch, n_s - s0);
+        __syncthreads();
+        // stage every (element of this CTA, scatterer of this pass) pair
+        for (int k = t; k < els * sn; k += SIM_UTHREADS) {
+            const int q = k / sn, j = k % sn;
+            const int64_t eq = min(e0 + q, n_el - 1);
+            const int p = s0 + j;
+            const double dx = pos[3 * p] - el[3 * eq], dy = pos[3 * p + 1] - el[3 * eq + 1],
+                         dz = pos[3 * p + 2] - el[3 * eq + 2];
+            const double d2 = -2.0 * sqrt(dx * dx + dy * dy + dz * dz);
+            s_d[q * ch + j] = d2;
+            s_step[q * ch + j] = cis_reduced(d2 * dk);
+            if (q == 0) s_r[j] = make_float2((float)refl[2 * p], (float)refl[2 * p + 1]);
+        }
+        __syncthreads();
+        if (live) {
+            const double *sd = s_d + le * ch;
+            const float2 *st = s_step + le * ch;
+            for (int j = 0; j < sn; ++j) {
+                float2 z = cmul(s_r[j], cis_reduced(sd[j] * kf0));
+                const float2 r = st[j];
+#pragma unroll
+                for (int i = 0; i < SIM_G; ++i) {
+                    acc[i].x += z.x;
+                    acc[i].y += z.y;
+                    if (i + 1 < SIM_G) z = cmul(z, r);
+                }
+            }
+        }
+    }
+    if (live)
+#pragma unroll
+        for (int i = 0; i < SIM_G; ++i)
+            if (f0 + i < n_f) out[e * n_f + f0 + i] = acc[i];
+}
+
 }  // namespace hhsar
 
 using namespace hhsar;
@@ -466,4 +538,19 @@ extern "C" int hhsar_simulate(const double *el_pos, int64_t n_el, const double *
     simulate_kernel<<<(unsigned)n_el, 256, 0, as_stream(stream)>>>(
         el_pos, pos, refl, (int)n_s, k, (int)n_f, reinterpret_cast<float2 *>(out));
     return check_launch("simulate_kernel");
+}
+
+extern "C" int hhsar_simulate_uniform(const double *el_pos, int64_t n_el, const double *pos,
+                                      const double *refl, int64_t n_s, double k0, double dk,
+                                      int64_t n_f, void *out, void *stream) {
+    HHSAR_REQUIRE(n_el >= 0 && n_s >= 0 && n_f >= 1 && n_f <= SIM_G * SIM_UTHREADS,
+                  "simulate_uniform: bad sizes (n_f must lie in [1, 2048])");
+    if (n_el == 0) return HHSAR_OK;
+    const int per_el = (int)((n_f + SIM_G - 1) / SIM_G);
+    const int els = SIM_UTHREADS / per_el;
+    const int64_t blocks = (n_el + els - 1) / els;
+    HHSAR_REQUIRE(blocks < (1ll << 31), "simulate_uniform: too many elements");
+    simulate_uniform_kernel<<<(unsigned)blocks, SIM_UTHREADS, 0, as_stream(stream)>>>(
+        el_pos, n_el, pos, refl, (int)n_s, k0, dk, (int)n_f, reinterpret_cast<float2 *>(out));
+    return check_launch("simulate_uniform_kernel");
 }
