@@ -126,6 +126,30 @@ class TorchComm:
             if r != self.rank:
                 buf[a:b] = recv[r * longest: r * longest + (b - a)]
 
+    def gather_segments(self, buf, segments, root: int = 0, base: int = 0) -> None:
+        """Like allgather_segments, but only ``root`` receives the other
+        ranks' segments (NCCL gather: root takes in (W-1)/W of the buffer,
+        the other ranks only send).  ``buf`` holds global indices from
+        ``base`` on (a non-root rank may pass just its own segment)."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        longest = max(b - a for a, b in segments)
+        a, b = segments[self.rank]
+        send = torch.zeros(longest, dtype=buf.dtype, device=buf.device)
+        send[:b - a] = buf[a - base:b - base]
+        if self.rank == root:
+            parts = [torch.empty(longest, dtype=buf.dtype, device=buf.device)
+                     for _ in range(self.world)]
+            dist.gather(self._raw(send), [self._raw(p) for p in parts], dst=root,
+                        group=self.group)
+            for r, (a, b) in enumerate(segments):
+                if r != self.rank:
+                    buf[a - base:b - base] = parts[r][:b - a]
+        else:
+            dist.gather(self._raw(send), None, dst=root, group=self.group)
+
 
 class EmulatedComm:
     """World of `world` ranks emulated by host threads in one process on one
@@ -154,6 +178,14 @@ class EmulatedComm:
         for p in parts[1:]:
             total += p
         t.copy_(total)
+
+    def gather_segments(self, buf, segments, root: int = 0, base: int = 0) -> None:
+        a, b = segments[self.rank]
+        parts = self._exchange(buf[a - base:b - base].clone())
+        if self.rank == root:
+            for r, (a, b) in enumerate(segments):
+                if r != self.rank:
+                    buf[a - base:b - base] = parts[r]
 
     def allgather_segments(self, buf, segments) -> None:
         a, b = segments[self.rank]
@@ -195,17 +227,44 @@ def plan_shard(n_elements: int, levels: int, merge_factor: int, world: int, rank
     return sched, kx, owned, (e0, e1)
 
 
+OUTPUTS = ("all", "root", "shard")
+
+
+def owned_elements(n_elements: int, levels: int, merge_factor: int = 2, comm=None):
+    """Element rows [e0, e1) whose echoes this rank needs (its subaperture
+    group): a multi-process caller loads only these rows and
+    passes them as ``rows=`` to hhffbpa_reconstruct_sharded."""
+    comm = comm or TorchComm()
+    return plan_shard(n_elements, levels, merge_factor, comm.world, comm.rank)[3]
+
+
 def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsample: int = 8,
-                                merge_factor: int = 2, comm=None):
+                                merge_factor: int = 2, comm=None, output: str = "all",
+                                rows=None):
     """hhffbpa_reconstruct (ffbp.py:415-513) over all ranks of `comm`
-    (default: torch.distributed's world).  Every rank returns the same
-    ImageVolume and provenance; each rank transfers and range-compresses only
-    its own subaperture group's echoes."""
+    (default: torch.distributed's world).  Each rank transfers and
+    range-compresses only its own subaperture group's echoes (streamed in
+    chunks, the compression overlapping the upload).
+
+    ``output`` -- where the volume lands:
+      "all"   every rank returns the whole ImageVolume (NCCL all-gather);
+      "root"  rank 0 returns the whole volume (NCCL gather), the others their
+              own x-slab;
+      "shard" every rank returns its own x-slab only (no volume collective;
+              the slabs tile the volume, see ``ShardedVolume``).
+    Provenance and error checks are identical on every rank in all modes.
+
+    ``rows``: this rank's echo rows [e0, e1) only (owned_elements()), e.g.
+    a pinned host buffer each process filled itself; ``cube.values`` is then
+    never read (each process holds 1/W of the cube).
+    """
     import torch
     from .bpa import _finish, check_delay_window, default_grid_dims, region_grid
     from .ffbp import FfbpParams, check_grids, default_levels, provenance_of
     from .model import partition_subarrays, validate_geometry
-    from .rangecomp import RangeProfileSet, profile_axis, to_device_cube
+    from .rangecomp import CubeUpload, RangeProfileSet, profile_axis
+    if output not in OUTPUTS:
+        raise ConfigError(f"output must be one of {OUTPUTS}")
     comm = comm or TorchComm()
     params = params or FfbpParams()
     validate_geometry(cube.aperture, region)
@@ -227,28 +286,51 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
                              upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
                              freqs=kgrid, elements_dev=el_dev)
     check_delay_window(window, region)
-    rows = to_device_cube(np.asarray(cube.values)[e0:e1])
-    vol, stats, flags, oow, sched, descs = hhffbpa_sharded_device(
-        comm, rows, e0, el_dev, kgrid, region, dims, params, levels, merge_factor, upsample)
-    if int(oow.cpu()[0]):  # a leaf delay outside the range gate (all-reduced: every rank agrees)
-        vol, stats, flags, oow, sched, descs = hhffbpa_sharded_device(
-            comm, rows, e0, el_dev, kgrid, region, dims, params, levels, merge_factor, upsample,
-            gate=False)
+    if rows is not None:
+        if tuple(rows.shape) != (e1 - e0, kgrid.count):
+            raise ConfigError(f"rows must hold this rank's elements [{e0}, {e1}) x "
+                              f"{kgrid.count} frequencies, got {tuple(rows.shape)}")
+        upload = CubeUpload(rows)
+        upload.row0 = e0
+        upload.chunks = [(a + e0, b + e0, ev) for a, b, ev in upload.chunks]
+    else:
+        upload = CubeUpload(cube.values, rows=(e0, e1))
+    res = hhffbpa_sharded_device(comm, upload.tensor, e0, el_dev, kgrid, region, dims, params,
+                                 levels, merge_factor, upsample, output=output, upload=upload)
+    if int(res.oow.cpu()[0]):  # a leaf delay outside the range gate (all-reduced: every rank agrees)
+        res = hhffbpa_sharded_device(comm, upload.tensor, e0, el_dev, kgrid, region, dims,
+                                     params, levels, merge_factor, upsample, gate=False,
+                                     output=output)
     origin, step = region_grid(region, dims)
-    extra = torch.cat([flags, stats.reshape(-1)])
-    volume, tail = _finish(vol, oow, dims, origin, step, {}, extra)
-    fl = tail[:flags.numel()]
-    st = tail[flags.numel():].reshape(-1, stats.shape[1])
-    run = SimpleNamespace(sched=sched, lattices=SimpleNamespace(descs=descs))
+    extra = torch.cat([res.flags, res.stats.reshape(-1)])
+    whole = output == "all" or (output == "root" and comm.rank == 0)
+    vol_dims = dims if whole else (res.vox_range[1] - res.vox_range[0], 1, 1)
+    volume, tail = _finish(res.volume, res.oow, vol_dims, origin, step, {}, extra)
+    fl = tail[:res.flags.numel()]
+    st = tail[res.flags.numel():].reshape(-1, res.stats.shape[1])
+    run = SimpleNamespace(sched=res.sched, lattices=SimpleNamespace(descs=res.descs))
     check_grids(run, st)
     prov = provenance_of(run, st, fl, dims, params, levels, upsample, merge_factor)
+    if not whole:
+        return ShardedVolume(values=volume.values.reshape(-1), vox_range=res.vox_range, dims=dims,
+                             origin=origin, step=step, provenance=prov)
     object.__setattr__(volume, "provenance", prov)
     return volume
 
 
+class ShardedVolume(SimpleNamespace):
+    """One rank's x-slab of a voxel-sharded volume: ``values`` complex64 for
+    the flattened [nx][ny][nz] indices ``vox_range`` = [vb, ve) of the whole
+    grid ``dims`` (origin / step as ImageVolume's); ``provenance`` is the
+    whole reconstruction's."""
+
+    def flat_indices(self):
+        return np.arange(*self.vox_range)
+
+
 def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, region, final_dims,
                            params, levels: int, merge_factor: int, upsample: int,
-                           gate: bool = True):
+                           gate: bool = True, output: str = "all", upload=None):
     """One rank's share of HHFFBPA:
 
     1. subaperture-group partition: the rank owns a contiguous run of
@@ -261,10 +343,14 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
        evaluates points;
     2. all-gather of the exchange level's downconverted lattices (NCCL);
     3. the few top merge levels redundantly on every rank;
-    4. the Cartesian landing voxel-sharded, then an all-gather of the slabs.
+    4. the Cartesian landing voxel-sharded, then (``output``) an all-gather
+       of the slabs ("all"), a gather to rank 0 ("root") or nothing
+       ("shard").
 
-    Returns (flat complex64 volume, stats[G,6], flags, oow) identical on all
-    ranks.
+    ``upload`` (rangecomp.CubeUpload of this rank's rows): compress chunk by
+    chunk as rows land.  Returns a namespace: volume (flat complex64: the
+    whole volume where it was gathered, else this rank's slab), vox_range,
+    stats[G,6], flags, oow (identical on all ranks), sched, descs.
     """
     import torch
     from .bpa import el_f32x4
@@ -284,8 +370,12 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
                          gate_dt=dt if gate else None, gate_bins=n_t)
     if gate:
         b0, w = lat.gate
-        env, t0, dt, k_ref = range_compress_window(cube_dev_rows, kgrid, upsample, b0, w)
+        env, t0, dt, k_ref = range_compress_window(
+            cube_dev_rows, kgrid, upsample, b0, w, chunks=upload.chunks if upload else None,
+            row0=e_row0)
     else:
+        if upload is not None:
+            upload.wait()
         env, dt, k_ref = range_compress_device(cube_dev_rows, kgrid, upsample)
         t0 = 0.0
     pipe = Pipeline(env, el_dev, el_f32x4(el_dev), t0, dt, k_ref, kgrid, region, final_dims,
@@ -308,9 +398,20 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     vb, ve = shard_range(n_vox, rank, world)
     part = pipe.land((vb, ve))
     # volume slabs
-    vol = torch.zeros(n_vox, dtype=torch.complex64, device=part.device)
-    vol[vb:ve] = part
-    comm.allgather_segments(vol, [shard_range(n_vox, r, world) for r in range(world)])
+    segs = [shard_range(n_vox, r, world) for r in range(world)]
+    if output == "all" or world == 1:
+        vol = torch.zeros(n_vox, dtype=torch.complex64, device=part.device)
+        vol[vb:ve] = part
+        comm.allgather_segments(vol, segs)
+    elif output == "root":
+        if rank == 0:
+            vol = torch.zeros(n_vox, dtype=torch.complex64, device=part.device)
+            vol[vb:ve] = part
+        else:
+            vol = part
+        comm.gather_segments(vol, segs, base=0 if rank == 0 else vb)
+    else:
+        vol = part
     # counters: rows / stages computed by owners are summed, redundant ones kept
     stats = pipe.lat.stats
     if world > 1 and kx >= 0:
@@ -331,7 +432,10 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         comm.allreduce_sum(fl)
         flags[pipe.n_stages:] = fl
         oow = pipe.oow
-    return vol, stats, flags, oow, sched, pipe.lat.descs
+    whole = output == "all" or world == 1 or (output == "root" and rank == 0)
+    return SimpleNamespace(volume=vol, vox_range=(0, n_vox) if whole else (vb, ve), stats=stats,
+                           flags=flags, oow=oow, sched=sched, descs=pipe.lat.descs)
+
 
 
 def _allreduce_sum(t, group=None):

@@ -38,7 +38,7 @@ from .bpa import (ImageVolume, _finish, bpa_volume_device, check_delay_window,
 from .errors import ConfigError, NumericDomainError
 from .model import (C_LIGHT, Subarray, boundary_lattice, leaf_bounds,
                     partition_subarrays, validate_geometry)
-from .rangecomp import RangeProfileSet, profile_axis, range_compress, to_device_cube
+from .rangecomp import CubeUpload, RangeProfileSet, profile_axis, range_compress, to_device_cube
 from .spectrum import TWO_PI, SubarrayExtents
 
 GRID_PAD = 2  # ffbp.py:32
@@ -509,7 +509,7 @@ def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
 
 def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
                       levels: int, merge_factor: int = 2, upsample: int = 8,
-                      vox_range=None, gate: bool = True) -> DeviceRun:
+                      vox_range=None, gate: bool = True, upload=None, marks=None) -> DeviceRun:
     """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
     high-priority side stream; once the plan's descriptors are on the host
     the range compression is launched on the caller's stream for the delay
@@ -519,6 +519,11 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     compression but shrinks the profiles to the leaf stage's reach (config
     2/3/4: 256/352/288 of 1,024/2,048/4,096 bins; config 4 68.7 GB of
     profiles -> 4.8 GB).
+
+    ``upload`` (a rangecomp.CubeUpload whose tensor is ``cube_dev``): the
+    cube is still crossing PCIe; the compression runs chunk by chunk as rows
+    land.  ``marks`` (a dict) receives CUDA events recorded on the caller's
+    stream around the range compression ("rc0", "rc1").
     """
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
@@ -537,7 +542,15 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
                                 src_pad_of(params), window_hi,
                                 gate_dt=dt if gate else None, gate_bins=n_t)
     newton_first = False
+    chunks = upload.chunks if upload is not None else None
+    if marks is not None:
+        marks["rc0"] = torch.cuda.Event(enable_timing=True)
+        marks["rc1"] = torch.cuda.Event(enable_timing=True)
     if not gate:
+        if upload is not None:
+            upload.wait(main)
+        if marks is not None:
+            marks["rc0"].record(main)
         env, dt, k_ref = range_compress_device(cube_dev, kgrid, upsample)
         t0 = 0.0
     else:
@@ -547,13 +560,21 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         # fix-up is the critical path and goes first
         pending["done"].synchronize()
         n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
-        newton_first = n_cols <= NEWTON_FIRST_MAX_COLUMNS
+        newton_first = n_cols <= NEWTON_FIRST_MAX_COLUMNS or upload is not None
         if newton_first:
             with torch.cuda.stream(geo):
                 lat = finish_lattices(pending)
         if _trace:
             _trace("gate")
-        env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w)
+        if marks is not None and not chunks:
+            marks["rc0"].record(main)
+        env, t0, dt, k_ref = range_compress_window(cube_dev, kgrid, upsample, b0, w,
+                                                   chunks=chunks,
+                                                   row0=upload.row0 if upload else 0)
+    if marks is not None:
+        if chunks and gate:
+            marks["rc0"] = None  # compression interleaved with the upload
+        marks["rc1"].record(main)
     if not newton_first:
         with torch.cuda.stream(geo):
             lat = finish_lattices(pending)
@@ -655,9 +676,13 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
     if region.z_min <= 0.0:
         raise ConfigError("region must sit strictly in front of the array")
     partition_subarrays(cube.aperture, levels)  # raises ConfigError when too deep
-    cube_dev = to_device_cube(cube.values)
+    # the cube streams in by chunks (pinned input: DMA straight from the
+    # caller's buffer) while the plan, Newton and the range compression of
+    # the rows already landed run
+    upload = CubeUpload(cube.values)
+    cube_dev = upload.tensor
     run = hhffbpa_from_cube(cube_dev, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
-                            params, levels, merge_factor, upsample)
+                            params, levels, merge_factor, upsample, upload=upload)
     if int(run.oow.cpu()[0]):
         # a leaf delay outside the range gate (the gate is a geometric bound;
         # this never fired on the BASELINE configs): redo on full profiles so

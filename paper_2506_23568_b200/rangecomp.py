@@ -17,6 +17,7 @@ backprojection kernel reads.
 from __future__ import annotations
 
 import os
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -74,19 +75,118 @@ def profile_axis(freqs, upsample: int):
     return n_t, dt, k_ref, (k_min - k_ref) * C_LIGHT
 
 
-def to_device_cube(values, device="cuda", stream=None):
-    """Host complex cube -> device complex64 (pinned staging, async copy)."""
+def _host_tensor(values):
     import torch
     if isinstance(values, torch.Tensor):
-        return values.to(device=device, dtype=torch.complex64, non_blocking=True)
+        return values
     arr = np.ascontiguousarray(values, dtype=np.complex64)
     with warnings.catch_warnings():  # read-only (frozen) arrays are only read here
         warnings.simplefilter("ignore", UserWarning)
-        host = torch.from_numpy(arr)
+        return torch.from_numpy(arr)
+
+
+def to_device_cube(values, device="cuda", stream=None):
+    """Host complex cube -> device complex64 (one copy; see upload_cube for
+    the chunked, overlappable form)."""
+    import torch
+    if isinstance(values, torch.Tensor):
+        return values.to(device=device, dtype=torch.complex64, non_blocking=True)
+    host = _host_tensor(values)
     if not host.is_pinned():
         # staging copy: pageable host memory cannot be DMA'd asynchronously
         return host.to(device)
     return host.to(device, non_blocking=True)
+
+
+_LOCAL = threading.local()  # per host thread: copy streams, pinned staging buffers
+UPLOAD_CHUNK_BYTES = 256 << 20
+
+
+def _local(name):
+    d = getattr(_LOCAL, name, None)
+    if d is None:
+        d = {}
+        setattr(_LOCAL, name, d)
+    return d
+
+
+def copy_stream(device):
+    """Per-device (and per host thread) stream for host->device uploads."""
+    import torch
+    streams = _local("streams")
+    key = torch.device(device).index
+    if key not in streams:
+        streams[key] = torch.cuda.Stream(device=device)
+    return streams[key]
+
+
+class CubeUpload:
+    """A cube on its way to the device: ``tensor`` (complex64 [rows, n_f] in
+    HBM) is filled chunk by chunk on a copy stream; ``chunks`` lists (r0, r1,
+    event) with the event recorded once rows [r0, r1) have landed, so
+    consumers (range compression) can start on early chunks while later
+    ones are still crossing PCIe.  Pinned host input is DMA'd directly
+    (every chunk queued at once); pageable input goes through two reused
+    pinned staging buffers (host copy of chunk i+1 overlaps the DMA of
+    chunk i)."""
+
+    def __init__(self, values, device="cuda", rows=None, chunk_bytes: int = UPLOAD_CHUNK_BYTES):
+        import torch
+        dev = torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        host = _host_tensor(values)
+        r0, r1 = rows if rows is not None else (0, host.shape[0])
+        n_f = host.shape[1]
+        self.row0 = r0
+        self.tensor = torch.empty((r1 - r0, n_f), dtype=torch.complex64, device=dev)
+        self.chunks = []
+        self.h2d_bytes = (r1 - r0) * n_f * 8
+        if r1 == r0:
+            return
+        step = max(1, int(chunk_bytes // (n_f * 8)))
+        cs = copy_stream(dev)
+        cs.wait_stream(torch.cuda.current_stream(dev))  # the destination is allocated
+        pinned = host.is_pinned() and host.dtype == torch.complex64
+        if pinned:
+            with torch.cuda.stream(cs):
+                for a in range(r0, r1, step):
+                    b = min(r1, a + step)
+                    self.tensor[a - r0:b - r0].copy_(host[a:b], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    self.chunks.append((a, b, ev))
+        else:
+            staging = _local("staging")
+            bufs = staging.get((dev.index, step, n_f))
+            if bufs is None:
+                bufs = [(torch.empty((step, n_f), dtype=torch.complex64, pin_memory=True),
+                         torch.cuda.Event()) for _ in range(2)]
+                staging.clear()
+                staging[(dev.index, step, n_f)] = bufs
+            src = host.numpy() if host.device.type == "cpu" else None
+            for i, a in enumerate(range(r0, r1, step)):
+                b = min(r1, a + step)
+                buf, free = bufs[i % 2]
+                free.synchronize()  # its previous DMA has finished
+                if src is not None:
+                    np.copyto(buf[:b - a].numpy(), src[a:b], casting="same_kind")
+                else:
+                    buf[:b - a].copy_(host[a:b])
+                with torch.cuda.stream(cs):
+                    self.tensor[a - r0:b - r0].copy_(buf[:b - a], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                free.record(cs)
+                self.chunks.append((a, b, ev))
+        self.tensor.record_stream(cs)
+
+    def wait(self, stream=None):
+        """Make ``stream`` (default: current) wait for every chunk."""
+        import torch
+        s = stream or torch.cuda.current_stream()
+        for _, _, ev in self.chunks:
+            s.wait_event(ev)
 
 
 def range_compress_device(cube_dev, freqs, upsample: int = 8):
@@ -112,21 +212,40 @@ def range_compress_device(cube_dev, freqs, upsample: int = 8):
     return prof, dt, k_ref
 
 
-def range_compress_window(cube_dev, freqs, upsample: int, b0: int, w: int):
+def range_compress_window(cube_dev, freqs, upsample: int, b0: int, w: int, out=None,
+                          chunks=None, row0: int = 0):
     """Device cube -> the delay-bin window [b0, b0 + w) of every envelope row
     (hhsar_range_compress_window).  Returns (envelopes [N_el, w], t0', dt,
-    k_ref): the gated rows are profiles starting at t0' = b0 dt."""
+    k_ref): the gated rows are profiles starting at t0' = b0 dt.
+
+    ``chunks`` (a CubeUpload's (r0, r1, event) list, rows counted from
+    ``row0``) compresses chunk by chunk, each launch waiting only for its
+    own rows to land, so the compression overlaps the rest of the upload."""
     import torch
     n_t, dt, k_ref, a = profile_axis(freqs, upsample)
     if not (16 <= n_t <= 8192 and n_t & (n_t - 1) == 0):
+        if chunks:
+            for *_, ev in chunks:
+                torch.cuda.current_stream().wait_event(ev)
         env, dt, k_ref = range_compress_device(cube_dev, freqs, upsample)
         return env[:, b0:b0 + w].contiguous(), b0 * dt, dt, k_ref
-    cube_dev = cube_dev.to(torch.complex64).contiguous()
-    prof = torch.empty((cube_dev.shape[0], w), dtype=torch.complex64, device=cube_dev.device)
-    _native.call("hhsar_range_compress_window", _native.ptr(cube_dev), cube_dev.shape[0],
-                 cube_dev.shape[1], n_t, a, dt, int(b0), int(w), _native.ptr(prof),
-                 _native.stream_handle())
-    return prof, b0 * dt, dt, k_ref
+    if cube_dev.dtype != torch.complex64:
+        cube_dev = cube_dev.to(torch.complex64)
+    cube_dev = cube_dev.contiguous()
+    if out is None:
+        out = torch.empty((cube_dev.shape[0], w), dtype=torch.complex64, device=cube_dev.device)
+    stream = torch.cuda.current_stream()
+    parts = [(r0 - row0, r1 - row0, ev) for r0, r1, ev in chunks] if chunks else \
+        [(0, cube_dev.shape[0], None)]
+    for r0, r1, ev in parts:
+        if ev is not None:
+            stream.wait_event(ev)
+        if r1 <= r0:
+            continue
+        _native.call("hhsar_range_compress_window", _native.c_void_p_offset(cube_dev, r0 * cube_dev.shape[1]),
+                     r1 - r0, cube_dev.shape[1], n_t, a, dt, int(b0), int(w),
+                     _native.c_void_p_offset(out, r0 * w), _native.stream_handle())
+    return out, b0 * dt, dt, k_ref
 
 
 def range_compress(cube, upsample: int = 8, device="cuda") -> RangeProfileSet:

@@ -65,13 +65,19 @@ def _comm_worker(rank, world, port, out_path):
     buf = torch.zeros(starts[-1], dtype=torch.complex64)
     a, b = starts[rank], starts[rank + 1]
     buf[a:b] = torch.arange(a, b, dtype=torch.float32) * (1 + 1j)
-    comm.allgather_segments(buf, list(zip(starts[:-1], starts[1:])))
+    segs = list(zip(starts[:-1], starts[1:]))
+    # gather to root: rank 0 passes the whole buffer, the others only their
+    # own segment (indexed from its start)
+    own = buf[a:b].clone()
+    root_buf = buf.clone() if rank == 0 else own
+    comm.gather_segments(root_buf, segs, base=0 if rank == 0 else a)
+    comm.allgather_segments(buf, segs)
     cnt = torch.tensor([rank + 1, 10 * rank], dtype=torch.int64)
     comm.allreduce_sum(cnt)
     # the subtree plan every rank derives must tile the leaves / elements
     plans = [plan_shard(1000, 8, 2, world, r) for r in range(world)]
     if rank == 0:
-        np.save(out_path, {"buf": buf.numpy(), "cnt": cnt.numpy(),
+        np.save(out_path, {"buf": buf.numpy(), "root": root_buf.numpy(), "cnt": cnt.numpy(),
                            "rows": [p[3] for p in plans], "kx": [p[1] for p in plans]},
                 allow_pickle=True)
     dist.barrier()
@@ -86,6 +92,7 @@ def test_comm_segments_allreduce_and_plan(tmp_path, world):
     res = np.load(out, allow_pickle=True).item()
     n = [0, 5, 17, 18, 30][world]
     assert np.array_equal(res["buf"], np.arange(n) * (1 + 1j))
+    assert np.array_equal(res["root"], np.arange(n) * (1 + 1j))
     assert list(res["cnt"]) == [sum(range(1, world + 1)), 10 * sum(range(world))]
     rows = res["rows"]
     assert rows[0][0] == 0 and rows[-1][1] == 1000

@@ -61,6 +61,35 @@ def test_sharded_hhffbpa_equals_single_gpu(case, world, levels, factor):
         assert vol.provenance == single.provenance
 
 
+@pytest.mark.parametrize("output", ["root", "shard"])
+def test_sharded_hhffbpa_output_modes(case, output):
+    """Gather-to-root and sharded output: rank 0 (root) or every rank
+    (shard) holds exactly its part of the single-GPU volume."""
+    import paper_2506_23568_b200 as hh
+    from paper_2506_23568_b200.dist import ShardedVolume, hhffbpa_reconstruct_sharded
+    w, cube = case
+    dims = (48, 48, 20)
+    params = hh.FfbpParams(levels=7)
+    single = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4, merge_factor=4)
+    world = 4
+    outs = _run_world(world, lambda comm: hhffbpa_reconstruct_sharded(
+        cube, w.region, dims, params, upsample=4, merge_factor=4, comm=comm, output=output))
+    flat = single.values.ravel()
+    covered = 0
+    for r, vol in enumerate(outs):
+        assert vol.provenance == single.provenance
+        if output == "root" and r == 0:
+            assert np.linalg.norm(vol.values - single.values) <= 1e-6 * np.linalg.norm(flat)
+            continue
+        assert isinstance(vol, ShardedVolume) and vol.dims == dims
+        vb, ve = vol.vox_range
+        covered += ve - vb
+        want = flat[vb:ve]
+        assert np.linalg.norm(vol.values - want) <= 1e-6 * np.linalg.norm(flat)
+    if output == "shard":
+        assert covered == flat.size
+
+
 def test_sharded_bpa_volume_equals_single_gpu(case):
     import paper_2506_23568_b200 as hh
     from paper_2506_23568_b200.dist import run_voxel_sharded
