@@ -241,24 +241,27 @@ def count_launches(fn):
 
 def _timed_steps(step, steps, warmup, barrier=None):
     """W untimed steps, then K steps bracketed by (barrier +) synchronize;
-    per-step device times from events on the current stream."""
+    per-step device times from events on the current stream.  Only the last
+    step's result is kept alive (holding every step's buffers would make
+    each step allocate fresh device memory -- cudaMalloc inside the timed
+    region); returns (mean ms, per-step ms, last result)."""
     import torch
+    out = None
     for _ in range(warmup):
-        step()
+        out = step()
     torch.cuda.synchronize()
     if barrier:
         barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     torch.cuda.synchronize()
     ev[0].record()
-    outs = []
     for i in range(steps):
-        outs.append(step())
+        out = step()
         ev[i + 1].record()
     torch.cuda.synchronize()
     total = ev[0].elapsed_time(ev[-1])
     per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
-    return total / steps, per, outs
+    return total / steps, per, out
 
 
 def _max_over_ranks(vals, world):
@@ -337,10 +340,9 @@ def run_ours(args):
 
     gpu = dev.index if world > 1 else int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0)
     with ClockSampler(gpu) as clocks:
-        ms, per_step, outs = _timed_steps(step, args.steps, args.warmup, barrier)
-    last = outs[-1]
-    oow = int((last.oow if world == 1 else last.oow).cpu()[0])
-    del outs
+        ms, per_step, last = _timed_steps(step, args.steps, args.warmup, barrier)
+    oow = int(last.oow.cpu()[0])
+    del last
     if oow:
         raise SystemExit("bench.py: a leaf delay fell outside the range gate (the timed step "
                          "would have dropped contributions)")
@@ -700,10 +702,10 @@ def hhffbpa_small_leg(index, dev, args):
     def step():
         return ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params,
                                       w.levels, w.merge_factor, w.upsample)
-    ms, per, outs = _timed_steps(step, steps, max(args.warmup, 3))
-    assert int(outs[-1].oow.cpu()[0]) == 0
-    path = hhffbpa_roofline(w, outs[-1], ms)
-    del outs
+    ms, per, last = _timed_steps(step, steps, max(args.warmup, 3))
+    assert int(last.oow.cpu()[0]) == 0
+    path = hhffbpa_roofline(w, last, ms)
+    del last
     host = torch.empty(cube.shape, dtype=torch.complex64, pin_memory=True)
     host.copy_(cube)
     data = DataCube(values=host.numpy(), aperture=w.aperture, freqs=w.freqs)
