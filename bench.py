@@ -533,7 +533,7 @@ def rc_roofline(w, run, rc_ms, step_ms):
         out["fft_fp32"] = {"tflops": round(flops / (kms / 1e3) / 1e12, 1),
                            "peak_tflops": round(fp32 / 1e12, 1),
                            "frac": round(flops / (kms / 1e3) / fp32, 3)}
-    traffic = _traffic("range_compress_kernel")
+    traffic = _traffic("range_compress_kernel_config4")
     out["traffic"] = traffic
     out["traffic_source"] = "profiles/traffic.json (ncu --set full dram read+write per launch)"
     return out

@@ -169,3 +169,50 @@ def read_volume(path):
     values = flat.reshape(dims[2], dims[1], dims[0]).transpose(2, 1, 0)
     return ImageVolume(values=values, origin=origin, step=step,
                        provenance=doc.get("provenance", {}))
+
+
+# ---- projection images and reports (io.py:166-234 formats) ------------------
+
+_PGM_DEPTHS = {8: (255, ">u1"), 16: (65535, ">u2")}
+
+
+def export_projection(image, path, depth: int = 8) -> None:
+    """A [0, 1] grayscale image (e.g. max_intensity_projection) as a binary
+    PGM ("P5"; 16-bit samples big-endian, the format's byte order)."""
+    img = np.asarray(image, dtype=np.float64)
+    if img.ndim != 2:
+        raise ConfigError("projection image must be 2-D")
+    if img.size == 0:
+        raise ConfigError("projection image is empty")
+    if not np.all(np.isfinite(img)) or img.min() < 0.0 or img.max() > 1.0:
+        raise ConfigError("projection values must lie in [0, 1]")
+    if depth not in _PGM_DEPTHS:
+        raise ConfigError("depth must be 8 or 16")
+    maxval, dtype = _PGM_DEPTHS[depth]
+    pixels = np.floor(img * maxval + 0.5).astype(dtype)
+    rows, cols = img.shape
+    Path(path).write_bytes(f"P5\n{cols} {rows}\n{maxval}\n".encode("ascii") + pixels.tobytes())
+
+
+def read_projection(path) -> np.ndarray:
+    """A binary PGM back to floats in [0, 1]."""
+    raw = Path(path).read_bytes()
+    fields = raw.split(b"\n", 3)
+    if len(fields) != 4 or fields[0] != b"P5":
+        raise IoFormatError(f"{path} is not a binary PGM")
+    try:
+        cols, rows = (int(v) for v in fields[1].split())
+        maxval = int(fields[2])
+    except ValueError as e:
+        raise IoFormatError(f"malformed PGM header in {path}: {e}") from e
+    wide = maxval >= 256
+    n = cols * rows * (2 if wide else 1)
+    if len(fields[3]) < n:
+        raise IoFormatError(f"truncated PGM payload in {path}")
+    pixels = np.frombuffer(fields[3][:n], dtype=">u2" if wide else ">u1")
+    return pixels.reshape(rows, cols).astype(np.float64) / maxval
+
+
+def write_report(path, report: dict) -> None:
+    """A key-value report as indented, key-sorted JSON (UTF-8)."""
+    Path(path).write_text(json.dumps(report, indent=1, sort_keys=True), encoding="utf-8")

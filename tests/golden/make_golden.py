@@ -20,6 +20,9 @@ config0  BASELINE config 0 (paper_2506_23568_b200.workloads.config(0)): BPA
          from reference primitives; all grid masks.
 metrics  metrics.py on seeded volumes/profiles (`make_golden.py metrics`
          regenerates only this one).
+cli_tools  the reference CLI's `project` (PGM, z/8-bit and x/16-bit) and
+         `metrics` (JSON report) on the io case's volumes
+         (`make_golden.py cli_tools`).
 """
 
 from __future__ import annotations
@@ -279,6 +282,22 @@ def case_io():
     np.savez_compressed(HERE / "io_reference.npz", **out)
 
 
+def case_cli_tools():
+    """The reference CLI's `project` and `metrics` subcommands on the io
+    case's volume (and a direct-BPA volume of the same cube): PGM bytes and
+    the JSON report the drop-in's subcommands must reproduce."""
+    from hhsar.cli import main as ref_main
+    cube_path, vol_path = HERE / "io_cube.bin", HERE / "io_vol.bin"
+    bpa_path = HERE / "io_bpa.bin"
+    assert ref_main(["reconstruct", "--algo", "bpa", "--in", str(cube_path), "--out",
+                     str(bpa_path), "--dims", "17,17,9"]) == 0
+    for axis, depth in (("z", 8), ("x", 16)):
+        assert ref_main(["project", "--in", str(vol_path), "--axis", axis, "--depth",
+                         str(depth), "--out", str(HERE / f"io_proj_{axis}{depth}.pgm")]) == 0
+    assert ref_main(["metrics", "--ref", str(bpa_path), "--test", str(vol_path),
+                     "--out", str(HERE / "io_metrics.json")]) == 0
+
+
 def case_metrics():
     """metrics.py outputs (psnr, max_intensity_projection, psf_metrics,
     profile_cut) on seeded volumes and profiles; error messages of the
@@ -338,7 +357,11 @@ def main():
     if sys.argv[1:] == ["metrics"]:
         case_metrics()
         return
+    if sys.argv[1:] == ["cli_tools"]:
+        case_cli_tools()
+        return
     case_io()
+    case_cli_tools()
     case_metrics()
     for name, fn in (("small", case_small), ("medium", case_medium), ("config0", case_config0)):
         out = {}

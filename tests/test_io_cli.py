@@ -142,3 +142,69 @@ def test_cli_simulate_matches_reference_cube(tmp_path):
     err = np.linalg.norm(got.values - want.values) / np.linalg.norm(want.values)
     assert err < 1e-6, err
     assert region == wregion
+
+
+# ---- project / metrics / bench subcommands and the PGM / report formats --------
+
+@pytest.mark.parametrize("name,depth", [("io_proj_z8.pgm", 8), ("io_proj_x16.pgm", 16)])
+def test_pgm_round_trip_of_reference_files(tmp_path, name, depth):
+    img = io.read_projection(GOLD / name)
+    assert img.min() >= 0.0 and img.max() == 1.0
+    out = tmp_path / name
+    io.export_projection(img, out, depth=depth)
+    assert out.read_bytes() == (GOLD / name).read_bytes()
+
+
+def test_pgm_and_report_validation(tmp_path):
+    with pytest.raises(ConfigError, match="must be 2-D"):
+        io.export_projection(np.zeros(4), tmp_path / "a.pgm")
+    with pytest.raises(ConfigError, match=r"lie in \[0, 1\]"):
+        io.export_projection(np.full((2, 2), 1.5), tmp_path / "a.pgm")
+    with pytest.raises(ConfigError, match="depth must be 8 or 16"):
+        io.export_projection(np.zeros((2, 2)), tmp_path / "a.pgm", depth=12)
+    (tmp_path / "bad.pgm").write_bytes(b"P2\n1 1\n255\n\x00")
+    with pytest.raises(IoFormatError, match="not a binary PGM"):
+        io.read_projection(tmp_path / "bad.pgm")
+    io.write_report(tmp_path / "r.json", {"b": 1, "a": [1.5]})
+    assert json.loads((tmp_path / "r.json").read_text()) == {"a": [1.5], "b": 1}
+
+
+def test_unexpected_errors_exit_1(tmp_path, capsys, monkeypatch):
+    def boom(args):
+        raise RuntimeError("boom")
+    monkeypatch.setattr(cli, "cmd_project", boom)
+    assert cli.main(["project", "--in", "x", "--out", str(tmp_path / "p.pgm")]) == 1
+    assert "unexpected error: RuntimeError: boom" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("axis,depth", [("z", 8), ("x", 16)])
+def test_cli_project_matches_reference_pgm(tmp_path, axis, depth):
+    out = tmp_path / "p.pgm"
+    assert cli.main(["project", "--in", str(GOLD / "io_vol.bin"), "--axis", axis, "--depth",
+                     str(depth), "--out", str(out)]) == 0
+    assert out.read_bytes() == (GOLD / f"io_proj_{axis}{depth}.pgm").read_bytes()
+
+
+@pytest.mark.gpu
+def test_cli_metrics_matches_reference_report(tmp_path):
+    out = tmp_path / "m.json"
+    assert cli.main(["metrics", "--ref", str(GOLD / "io_bpa.bin"), "--test",
+                     str(GOLD / "io_vol.bin"), "--out", str(out)]) == 0
+    got = json.loads(out.read_text())
+    want = json.loads((GOLD / "io_metrics.json").read_text())
+    assert set(got) == set(want)
+    assert abs(got["psnr_db"] - want["psnr_db"]) < 1e-6
+
+
+@pytest.mark.gpu
+def test_cli_bench_sweep_csv(tmp_path):
+    out = tmp_path / "b.csv"
+    assert cli.main(["bench", "--config", str(GOLD / "run_config.json"), "--sizes", "9,13",
+                     "--out", str(out)]) == 0
+    rows = out.read_text().splitlines()
+    assert rows[0] == "size,algo,seconds,predicted_ops"
+    body = [r.split(",") for r in rows[1:]]
+    assert [(r[0], r[1]) for r in body] == [("9", "bpa"), ("9", "hhffbpa"), ("13", "bpa"),
+                                            ("13", "hhffbpa")]
+    assert all(float(r[2]) > 0 and float(r[3]) > 0 for r in body)
