@@ -261,7 +261,7 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
     import torch
     from .bpa import _finish, check_delay_window, default_grid_dims, region_grid
     from .ffbp import FfbpParams, check_grids, default_levels, provenance_of
-    from .model import partition_subarrays, validate_geometry
+    from .model import leaf_bounds, validate_geometry
     from .rangecomp import CubeUpload, RangeProfileSet, profile_axis
     if output not in OUTPUTS:
         raise ConfigError(f"output must be one of {OUTPUTS}")
@@ -276,7 +276,7 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
                           "use bpa_reconstruct_sharded)")
     if region.z_min <= 0.0:
         raise ConfigError("region must sit strictly in front of the array")
-    partition_subarrays(cube.aperture, levels)
+    leaf_bounds(cube.aperture.n_elements, levels)  # ConfigError when too deep
     n_el = cube.aperture.n_elements
     _, _, _, (e0, e1) = plan_shard(n_el, levels, merge_factor, comm.world, comm.rank)
     el_dev = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
@@ -286,19 +286,28 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
                              upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
                              freqs=kgrid, elements_dev=el_dev)
     check_delay_window(window, region)
-    if rows is not None:
-        if tuple(rows.shape) != (e1 - e0, kgrid.count):
-            raise ConfigError(f"rows must hold this rank's elements [{e0}, {e1}) x "
-                              f"{kgrid.count} frequencies, got {tuple(rows.shape)}")
-        upload = CubeUpload(rows)
-        upload.row0 = e0
-        upload.chunks = [(a + e0, b + e0, ev) for a, b, ev in upload.chunks]
-    else:
-        upload = CubeUpload(cube.values, rows=(e0, e1))
-    res = hhffbpa_sharded_device(comm, upload.tensor, e0, el_dev, kgrid, region, dims, params,
-                                 levels, merge_factor, upsample, output=output, upload=upload)
+    if rows is not None and tuple(rows.shape) != (e1 - e0, kgrid.count):
+        raise ConfigError(f"rows must hold this rank's elements [{e0}, {e1}) x "
+                          f"{kgrid.count} frequencies, got {tuple(rows.shape)}")
+    uploads = []
+
+    def start_upload():
+        # started once the plan's small copy is queued (it must not wait behind
+        # the cube's chunks in the copy engine)
+        if rows is not None:
+            up = CubeUpload(rows)
+            up.row0 = e0
+            up.chunks = [(a + e0, b + e0, ev) for a, b, ev in up.chunks]
+        else:
+            up = CubeUpload(cube.values, rows=(e0, e1))
+        uploads.append(up)
+        return up
+
+    res = hhffbpa_sharded_device(comm, None, e0, el_dev, kgrid, region, dims, params,
+                                 levels, merge_factor, upsample, output=output,
+                                 upload=start_upload)
     if int(res.oow.cpu()[0]):  # a leaf delay outside the range gate (all-reduced: every rank agrees)
-        res = hhffbpa_sharded_device(comm, upload.tensor, e0, el_dev, kgrid, region, dims,
+        res = hhffbpa_sharded_device(comm, uploads[0].tensor, e0, el_dev, kgrid, region, dims,
                                      params, levels, merge_factor, upsample, gate=False,
                                      output=output)
     origin, step = region_grid(region, dims)
@@ -347,14 +356,15 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
        of the slabs ("all"), a gather to rank 0 ("root") or nothing
        ("shard").
 
-    ``upload`` (rangecomp.CubeUpload of this rank's rows): compress chunk by
-    chunk as rows land.  Returns a namespace: volume (flat complex64: the
+    ``upload`` (rangecomp.CubeUpload of this rank's rows, or a zero-argument
+    factory of one started right after the plan is queued; ``cube_dev_rows``
+    may then be None): compress chunk by chunk as rows land.  Returns a namespace: volume (flat complex64: the
     whole volume where it was gathered, else this rank's slab), vox_range,
     stats[G,6], flags, oow (identical on all ranks), sched, descs.
     """
     import torch
     from .bpa import el_f32x4
-    from .ffbp import Pipeline, build_lattices, src_pad_of
+    from .ffbp import Pipeline, finish_lattices, plan_lattices, src_pad_of
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     world, rank = comm.world, comm.rank
     sched, kx, owned, _ = plan_shard(el_dev.shape[0], levels, merge_factor, world, rank)
@@ -365,9 +375,13 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         mask[a:b] = True
     n_t, dt, _, _ = profile_axis(kgrid, upsample)
     window_hi = (n_t - 1) * dt
-    lat = build_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
-                         src_pad_of(params), window_hi, newton_grids=mask,
-                         gate_dt=dt if gate else None, gate_bins=n_t)
+    pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
+                            src_pad_of(params), window_hi, gate_dt=dt if gate else None,
+                            gate_bins=n_t)
+    if callable(upload):
+        upload = upload()
+        cube_dev_rows = upload.tensor
+    lat = finish_lattices(pending, newton_grids=mask)
     if gate:
         b0, w = lat.gate
         env, t0, dt, k_ref = range_compress_window(

@@ -520,9 +520,12 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     2/3/4: 256/352/288 of 1,024/2,048/4,096 bins; config 4 68.7 GB of
     profiles -> 4.8 GB).
 
-    ``upload`` (a rangecomp.CubeUpload whose tensor is ``cube_dev``): the
-    cube is still crossing PCIe; the compression runs chunk by chunk as rows
-    land.  ``marks`` (a dict) receives CUDA events recorded on the caller's
+    ``upload`` (a rangecomp.CubeUpload whose tensor is ``cube_dev``, or a
+    zero-argument factory of one, then ``cube_dev`` may be None): the cube is
+    still crossing PCIe; the compression runs chunk by chunk as rows land.
+    A factory is called right after the plan's small host->device copy is
+    queued, so that copy does not wait behind gigabytes of cube chunks in
+    the copy engine (the plan's round trip gates the compression).  ``marks`` (a dict) receives CUDA events recorded on the caller's
     stream around the range compression ("rc0", "rc1").
     """
     import torch
@@ -532,7 +535,7 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
     window_hi = 0.0 + (n_t - 1) * dt
     main = torch.cuda.current_stream()
-    geo = geometry_stream(cube_dev.device)
+    geo = geometry_stream(el_dev.device)
     geo.wait_stream(main)
     sched = Schedule.shared(int(el_dev.shape[0]), levels, merge_factor)
     if _trace:
@@ -541,6 +544,9 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi,
                                 gate_dt=dt if gate else None, gate_bins=n_t)
+    if callable(upload):
+        upload = upload()
+        cube_dev = upload.tensor
     newton_first = False
     chunks = upload.chunks if upload is not None else None
     if marks is not None:
@@ -589,9 +595,8 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     return pipe.run(vox_range)
 
 
-def _core_masked(desc, n_valid_core) -> float:
-    size = int(np.prod(desc["core_hi"].astype(np.int64) - desc["core_lo"] + 1))
-    return 1.0 - (int(n_valid_core) / size)
+def _core_sizes(descs) -> np.ndarray:
+    return np.prod(descs["core_hi"].astype(np.int64) - descs["core_lo"] + 1, axis=1)
 
 
 def _raise_core(masked: float):
@@ -603,19 +608,19 @@ def _raise_core(masked: float):
 def check_grids(run: DeviceRun, stats: np.ndarray):
     """The reference's SubimageGrid health checks (ffbp.py:127-133) in the
     reference's order: each leaf as built, then after its delay mask
-    (ffbp.py:331-335), then every parent level by level."""
+    (ffbp.py:331-335), then every parent level by level (vectorised: the
+    first failing grid in that order raises)."""
     sched, descs = run.sched, run.lattices.descs
+    size = _core_sizes(descs)
     g0, g1 = sched.level_slices[0]
-    for g in range(g0, g1):
-        for col in (1, 3):
-            m = _core_masked(descs[g], stats[g, col])
-            if m >= 0.5:
-                _raise_core(m)
-    for (a, b) in sched.level_slices[1:]:
-        for g in range(a, b):
-            m = _core_masked(descs[g], stats[g, 1])
-            if m >= 0.5:
-                _raise_core(m)
+    # leaves: [built, masked] interleaved per grid, then the parents in order
+    leaf = np.stack([1.0 - stats[g0:g1, 1] / size[g0:g1],
+                     1.0 - stats[g0:g1, 3] / size[g0:g1]], axis=1).reshape(-1)
+    parents = 1.0 - stats[g1:, 1] / size[g1:]
+    masked = np.concatenate([leaf, parents])
+    bad = np.flatnonzero(masked >= 0.5)
+    if bad.size:
+        _raise_core(float(masked[bad[0]]))
 
 
 def provenance_of(run: DeviceRun, stats, flags, final_dims, params, levels, upsample,
@@ -675,14 +680,19 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
                                        freqs=kgrid, elements_dev=el_dev), region)
     if region.z_min <= 0.0:
         raise ConfigError("region must sit strictly in front of the array")
-    partition_subarrays(cube.aperture, levels)  # raises ConfigError when too deep
+    leaf_bounds(cube.aperture.n_elements, levels)  # ConfigError when too deep (model.py:371-376)
     # the cube streams in by chunks (pinned input: DMA straight from the
     # caller's buffer) while the plan, Newton and the range compression of
     # the rows already landed run
-    upload = CubeUpload(cube.values)
-    cube_dev = upload.tensor
-    run = hhffbpa_from_cube(cube_dev, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
-                            params, levels, merge_factor, upsample, upload=upload)
+    uploads = []
+
+    def start_upload():
+        uploads.append(CubeUpload(cube.values))
+        return uploads[0]
+
+    run = hhffbpa_from_cube(None, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
+                            params, levels, merge_factor, upsample, upload=start_upload)
+    cube_dev = uploads[0].tensor
     if int(run.oow.cpu()[0]):
         # a leaf delay outside the range gate (the gate is a geometric bound;
         # this never fired on the BASELINE configs): redo on full profiles so

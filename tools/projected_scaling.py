@@ -7,7 +7,11 @@ stated NVLink bandwidth.  Projected time at world W = max over ranks of the
 rank's device time + exchange bytes / bandwidth.
 
     python tools/projected_scaling.py 3 2 4 8     (config, worlds...)
+    OUTPUT=all|root|shard python tools/projected_scaling.py 4 2 4 8
+      (volume output mode of dist.hhffbpa_sharded_device; default shard,
+      the bench's N > 1 mode)
 """
+import os
 import json
 import sys
 from pathlib import Path
@@ -36,6 +40,14 @@ class CountingComm:
         longest = max(b - a for a, b in segments)
         self.bytes += longest * buf.element_size() * (self.world - 1)
 
+    def gather_segments(self, buf, segments, root=0, base=0):
+        # the root receives W-1 segments; the others send one
+        longest = max(b - a for a, b in segments)
+        self.bytes += longest * buf.element_size() * ((self.world - 1) if self.rank == root else 1)
+
+
+OUTPUT = os.environ.get("OUTPUT", "shard")
+
 
 def time_rank(w, cube, el, params, factor, world, rank, reps=3):
     sched, kx, owned, (e0, e1) = dist.plan_shard(w.n_elements, w.levels, factor, world, rank)
@@ -46,7 +58,7 @@ def time_rank(w, cube, el, params, factor, world, rank, reps=3):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         dist.hhffbpa_sharded_device(comm, rows, e0, el, w.freqs, w.region, w.dims, params,
-                                    w.levels, factor, w.upsample)
+                                    w.levels, factor, w.upsample, output=OUTPUT)
         e.record()
         torch.cuda.synchronize()
         t = s.elapsed_time(e)
@@ -66,7 +78,7 @@ def main():
     params = ffbp.FfbpParams(levels=w.levels)
     t1, _ = time_rank(w, cube, el, params, factor, 1, 0)
     out = {"config": cfg, "merge_factor": factor, "one_gpu_ms": round(t1, 3),
-           "nvlink_gbs_assumed": NVLINK_GBS, "note": "projection: ranks timed one at a time "
+           "nvlink_gbs_assumed": NVLINK_GBS, "output": OUTPUT, "note": "projection: ranks timed one at a time "
            "on one B200, collectives costed from bytes", "worlds": {}}
     for W in worlds:
         per = [time_rank(w, cube, el, params, factor, W, r) for r in range(W)]
