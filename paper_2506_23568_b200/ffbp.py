@@ -249,12 +249,17 @@ def _region_tuple(region):
 
 def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: float, pad: int,
                   window_hi: float, tol: float = 1e-9, max_iter: int = 50, gate_dt=None,
-                  gate_bins: int = 0):
+                  gate_bins: int = 0, cached=None):
     """Launch the leaf boxes + plan kernels and the asynchronous readback of
     the descriptors (pinned) on the current stream; returns a pending plan
     for finish_lattices (which is the only host wait).  With ``gate_dt``
     (profile bin width) and ``gate_bins`` (profile length) the leaf range
-    gate (hhsar_leaf_range_gate) comes back with the plan as lat.gate."""
+    gate (hhsar_leaf_range_gate) comes back with the plan as lat.gate.
+
+    ``cached`` (a PlanCache of an earlier plan of the SAME geometry): the
+    plan kernels still run, but nothing is read back -- the host takes the
+    descriptors and sizes from the cache, so no host wait remains and the
+    step can be captured in a CUDA graph (StepGraph)."""
     import ctypes
     import torch
     dev = el_dev.device
@@ -283,6 +288,10 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
                      ctypes.c_void_p(descs_dev.data_ptr() + a * _native.GRID_DTYPE.itemsize),
                      b - a, float(gate_dt), int(gate_bins), _native.c_void_p_offset(status, 24),
                      stream)
+    if cached is not None:
+        return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
+                    host_d=None, host_s=cached.status, done=None, back=None,
+                    keep=(staged, up, leaf_box), cached=cached)
     back = torch.empty(int(cuts[1]) + 40, dtype=torch.uint8, pin_memory=True)
     back[:cuts[1]].copy_(descs_dev, non_blocking=True)
     back[cuts[1]:].copy_(status, non_blocking=True)
@@ -290,7 +299,7 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     done.record()
     return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
                 host_d=back[:cuts[1]], host_s=back[cuts[1]:].numpy(),
-                done=done, back=back, keep=(staged, up, leaf_box))
+                done=done, back=back, keep=(staged, up, leaf_box), cached=None)
 
 
 _trace = None  # optional host-timeline hook (tools/host_overhead.py)
@@ -299,15 +308,23 @@ _trace = None  # optional host-timeline hook (tools/host_overhead.py)
 def finish_lattices(p, newton_grids=None) -> Lattices:
     """Wait for the plan, size the pools, launch Newton (current stream)."""
     import torch
-    p["done"].synchronize()
+    cached = p.get("cached")
+    if cached is None:
+        p["done"].synchronize()
     if _trace:
         _trace("plan synced")
     sched, descs_dev, geom = p["sched"], p["descs_dev"], p["geom"]
     dev = descs_dev.device
     stream = _native.stream_handle()
     # the plan's pinned read-back IS the host descriptor table from here on
-    # (edited in place, uploaded from, kept alive with the lattices)
-    host = p["host_d"].numpy().view(_native.GRID_DTYPE)
+    # (edited in place, uploaded from, kept alive with the lattices); a
+    # cached plan brings its own copy
+    if cached is not None:
+        if newton_grids is not None:
+            raise ValueError("a cached plan covers the whole schedule (no newton_grids)")
+        host = cached.descs
+    else:
+        host = p["host_d"].numpy().view(_native.GRID_DTYPE)
     status = p["host_s"]
     if int(status[:4].view(np.int32)[0]):
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
@@ -341,6 +358,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     lat = Lattices(host, descs_dev, positions, valid, stats, geom)
     lat.keep = (p["back"], p["keep"][1])  # pinned staging must outlive the async copy
     lat.gate = (g_b0, g_w) if g_w > 0 else None
+    lat.status = status
     return lat
 
 
@@ -509,7 +527,8 @@ def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
 
 def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: FfbpParams,
                       levels: int, merge_factor: int = 2, upsample: int = 8,
-                      vox_range=None, gate: bool = True, upload=None, marks=None) -> DeviceRun:
+                      vox_range=None, gate: bool = True, upload=None, marks=None,
+                      plan_cache=None) -> DeviceRun:
     """Whole HHFFBPA step from a device cube.  Plan + Newton run on a
     high-priority side stream; once the plan's descriptors are on the host
     the range compression is launched on the caller's stream for the delay
@@ -525,8 +544,11 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     still crossing PCIe; the compression runs chunk by chunk as rows land.
     A factory is called right after the plan's small host->device copy is
     queued, so that copy does not wait behind gigabytes of cube chunks in
-    the copy engine (the plan's round trip gates the compression).  ``marks`` (a dict) receives CUDA events recorded on the caller's
-    stream around the range compression ("rc0", "rc1").
+    the copy engine (the plan's round trip gates the compression).
+    ``marks`` (a dict) receives CUDA events recorded on the caller's stream
+    around the range compression ("rc0", "rc1").  ``plan_cache`` (PlanCache
+    of an earlier step of the same geometry): no host wait at all (see
+    plan_lattices) -- the form StepGraph captures.
     """
     import torch
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
@@ -543,7 +565,7 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi,
-                                gate_dt=dt if gate else None, gate_bins=n_t)
+                                gate_dt=dt if gate else None, gate_bins=n_t, cached=plan_cache)
     if callable(upload):
         upload = upload()
         cube_dev = upload.tensor
@@ -564,7 +586,8 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
         # compression goes first (it fills the GPU while the host sizes the
         # pools and launches Newton); on small ones Newton's latency-bound
         # fix-up is the critical path and goes first
-        pending["done"].synchronize()
+        if plan_cache is None:
+            pending["done"].synchronize()
         n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
         newton_first = n_cols <= NEWTON_FIRST_MAX_COLUMNS or upload is not None
         if newton_first:
@@ -593,6 +616,69 @@ def hhffbpa_from_cube(cube_dev, el_dev, el4, kgrid, region, final_dims, params: 
     if _trace:
         _trace("pipeline ready")
     return pipe.run(vox_range)
+
+
+@dataclass
+class PlanCache:
+    """Host copy of a plan (descriptor table + status words) for one
+    geometry: the plan is a pure function of the element positions, the
+    region, the band and the parameters, so a later step of the same
+    geometry can size its pools and launches from it without waiting for
+    its own (recomputed) plan."""
+    descs: np.ndarray   # GRID_DTYPE [G] (pool / work-list offsets filled in)
+    status: np.ndarray  # uint8 [40]: status word, totals, gate
+
+    @staticmethod
+    def of(run: DeviceRun) -> "PlanCache":
+        lat = run.lattices
+        return PlanCache(descs=lat.descs.copy(), status=np.asarray(lat.status).copy())
+
+
+class StepGraph:
+    """One HHFFBPA step (hhffbpa_from_cube) captured in a CUDA graph.
+
+    Small configs are launch- and latency-bound: config 2's step is ~60
+    launches and one plan round trip.  An eager step first records the plan
+    (PlanCache); a second eager step with the cached plan checks the result
+    is bit-identical to the first; then the same host sequence -- plan,
+    Newton (with its side-stream fix-up), gated compression, leaves, merges,
+    landing, every kernel recomputed -- is captured once and replayed.
+    Fixed per graph: the geometry (element positions, region, band,
+    parameters) and the cube buffer's address; the cube's contents may
+    change between replays.  ``replay()`` returns the DeviceRun whose
+    tensors the graph rewrites each time."""
+
+    def __init__(self, cube_dev, el_dev, el4, kgrid, region, final_dims, params, levels,
+                 merge_factor=2, upsample=8, vox_range=None):
+        import torch
+        args = (cube_dev, el_dev, el4, kgrid, region, final_dims, params, levels, merge_factor,
+                upsample, vox_range)
+        first = hhffbpa_from_cube(*args)
+        torch.cuda.synchronize()
+        if int(first.oow.cpu()[0]):
+            raise NumericDomainError("leaf delays outside the range gate: use "
+                                     "hhffbpa_reconstruct, which redoes the step ungated")
+        self.cache = PlanCache.of(first)
+        check = hhffbpa_from_cube(*args, plan_cache=self.cache)
+        torch.cuda.synchronize()
+        if not (torch.equal(check.volume, first.volume) and
+                torch.equal(check.lattices.stats, first.lattices.stats)):
+            raise RuntimeError("cached-plan step differs from the planned step")
+        del first, check
+        side = torch.cuda.Stream(device=el_dev.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # capture-safe warm-up on a side stream
+            hhffbpa_from_cube(*args, plan_cache=self.cache)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.run = hhffbpa_from_cube(*args, plan_cache=self.cache)
+        self._args = args  # the captured buffers stay alive with the graph
+
+    def replay(self) -> DeviceRun:
+        self.graph.replay()
+        return self.run
 
 
 def _core_sizes(descs) -> np.ndarray:

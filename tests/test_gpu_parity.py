@@ -374,3 +374,32 @@ def test_range_gate_matches_full_profiles(config):
     assert torch.equal(runs[0].flags, runs[1].flags)
     n_t, dt, _, _ = rangecomp.profile_axis(w.freqs, w.upsample)
     assert runs[1].lattices.gate == ffbp.leaf_range_gate(runs[1].lattices, runs[1].sched, dt, n_t)
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_step_graph_replays_the_eager_step(config):
+    """StepGraph (plan cache + CUDA graph of the whole HHFFBPA step):
+    replays are bit-identical to the eager step, follow the cube's contents
+    (same graph, new data) and keep provenance counters identical."""
+    import torch
+    from paper_2506_23568_b200 import bpa, ffbp, workloads
+    w = workloads.config(config)
+    gen = torch.Generator(device="cuda").manual_seed(w.seed)
+    cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
+                       generator=gen)
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    el4 = bpa.el_f32x4(el)
+    params = ffbp.FfbpParams(levels=w.levels)
+    args = (el, el4, w.freqs, w.region, w.dims, params, w.levels, w.merge_factor, w.upsample)
+    g = ffbp.StepGraph(cube, *args)
+    eager = ffbp.hhffbpa_from_cube(cube, *args)
+    run = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(run.volume, eager.volume)
+    assert torch.equal(run.lattices.stats, eager.lattices.stats)
+    assert torch.equal(run.flags, eager.flags)
+    cube.mul_(0.5 - 2.0j)  # new data, same buffer: the replay must follow it
+    eager2 = ffbp.hhffbpa_from_cube(cube, *args)
+    run = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(run.volume, eager2.volume)
