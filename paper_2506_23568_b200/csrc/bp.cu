@@ -80,16 +80,20 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
                 int nz, int64_t vb, int64_t ve, const float4 *__restrict__ el, int m,
                 const float2 *__restrict__ env, BpFast k, float2 *__restrict__ out,
                 int64_t *__restrict__ oow_total, int tx_base, int n_tiles, int split,
-                float2 *__restrict__ part, const float2 *__restrict__ rot) {
+                float2 *__restrict__ part, int *__restrict__ arrivals,
+                const float2 *__restrict__ rot) {
     constexpr int TL_VX = VX;  // voxels per thread along x
     __shared__ float4 s_env[TL_CHUNK * TL_W];  // 32 KB
     __shared__ float4 s_el[TL_CHUNK];          // x, y, z, bits(byte offset | -1 = slow)
     __shared__ int s_lo[TL_CHUNK];
     const int tiles_z = (nz + TL_TZ - 1) / TL_TZ, tiles_y = (ny + TL_TY - 1) / TL_TY;
-    // work item = (element split s, tile); all tiles of split 0 first so the
-    // concurrently resident CTAs stream the same elements (L2 reuse)
-    const int sidx = blockIdx.x / n_tiles;
-    const int b = blockIdx.x % n_tiles;
+    // work item = (tile, element split s), tile-major: a tile's split CTAs
+    // run at about the same time, so the partial-sum slabs they exchange
+    // (below) live only briefly in L2; the envelope rows the resident CTAs
+    // read at any moment stay a few MB (every CTA walks its element range
+    // in step with the others)
+    const int sidx = blockIdx.x % split;
+    const int b = blockIdx.x / split;
     const int tz = b % tiles_z, ty = (b / tiles_z) % tiles_y;
     const int tx = tx_base + b / (tiles_z * tiles_y);
     const int per = ((m + split - 1) / split + TL_CHUNK - 1) / TL_CHUNK * TL_CHUNK;
@@ -253,31 +257,60 @@ bpa_tile_kernel(double ox, double oy, double oz, double sx, double sy, double sz
             }
         }
     }
-    float2 *dst = sidx == 0 ? out : part + (int64_t)(sidx - 1) * (ve - vb);
+    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
+    float2 mine[TL_VX];
 #pragma unroll
     for (int v = 0; v < TL_VX; ++v) {
-        if (!live_of(v)) continue;
         if constexpr (PAIR)
-            dst[flat_of(v) - vb] = make_float2(lo2(pa[v]) - hi2(pb[v]), hi2(pa[v]) + lo2(pb[v]));
+            mine[v] = make_float2(lo2(pa[v]) - hi2(pb[v]), hi2(pa[v]) + lo2(pb[v]));
         else
-            dst[flat_of(v) - vb] = acc[v];
+            mine[v] = acc[v];
     }
-    if (bad) atomicAdd((unsigned long long *)oow_total, (unsigned long long)bad);
-}
-
-// out[i] += part[0][i] + part[1][i] + ... (fixed order: deterministic)
-__global__ void add_parts_kernel(float2 *__restrict__ out, const float2 *__restrict__ part,
-                                 int n_parts, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float2 a = out[i];
-        for (int p = 0; p < n_parts; ++p) {
-            const float2 b = part[(int64_t)p * n + i];
-            a.x += b.x;
-            a.y += b.y;
+    if (split == 1) {
+#pragma unroll
+        for (int v = 0; v < TL_VX; ++v)
+            if (live_of(v)) out[flat_of(v) - vb] = mine[v];
+        return;
+    }
+    // split > 1: the tile's CTAs each park their partial sums (8 KB) in a
+    // per-tile scratch slab; the LAST one to finish (per-tile arrival counter)
+    // adds the slabs in split order -- deterministic, no second kernel, and
+    // the slabs live only as long as the tile is in flight, so they stay in
+    // L2 instead of round-tripping through HBM
+    constexpr int SLOTS = TL_THREADS * TL_VX;
+    float2 *slab = part + ((int64_t)b * split + sidx) * SLOTS;
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v) slab[t * TL_VX + v] = mine[v];
+    __threadfence();
+    __shared__ int s_last;
+    __syncthreads();
+    if (t == 0) s_last = atomicAdd(arrivals + b, 1) == split - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();  // every other slab of the tile is visible
+    float2 sum[TL_VX];
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v) sum[v] = make_float2(0.f, 0.f);
+    for (int r = 0; r < split; ++r) {
+        const float2 *src = part + ((int64_t)b * split + r) * SLOTS + t * TL_VX;
+#pragma unroll
+        for (int v = 0; v < TL_VX; ++v) {
+            const float2 p = r == sidx ? mine[v] : __ldcg(src + v);
+            sum[v].x += p.x;
+            sum[v].y += p.y;
         }
-        out[i] = a;
     }
+#pragma unroll
+    for (int v = 0; v < TL_VX; ++v)
+        if (live_of(v)) out[flat_of(v) - vb] = sum[v];
+    // the slabs are dead: drop their L2 lines without writing them back
+    // (discard.global.L2), so the scratch never reaches HBM
+    __syncthreads();  // every thread of this CTA has read the slabs
+    constexpr int LINES = SLOTS * (int)sizeof(float2) / 128;  // per slab
+    const char *tile_slabs = reinterpret_cast<const char *>(part + (int64_t)b * split * SLOTS);
+    for (int l = t; l < split * LINES; l += TL_THREADS)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(tile_slabs + (int64_t)l * 128)
+                     : "memory");
 }
 
 // Generic gather for arbitrary points (operator-level backproject_gather).
@@ -371,16 +404,20 @@ int launch_tile(const TileArgs &a) {
     const int64_t tiles = (int64_t)(tx1 - tx0 + 1) * per_x;
     const int split = tile_split(tiles, a.m, per_sm);
     float2 *part = nullptr;
-    const int64_t nv = a.ve - a.vb;
-    if (split > 1 && cudaMallocAsync(&part, (split - 1) * nv * sizeof(float2), a.s) != cudaSuccess)
-        return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
+    int *arrivals = nullptr;
+    if (split > 1) {
+        const size_t slab = (size_t)TL_THREADS * VX * sizeof(float2);
+        if (cudaMallocAsync(&part, (size_t)tiles * split * slab + tiles * sizeof(int), a.s) !=
+            cudaSuccess)
+            return set_error(HHSAR_ECUDA, "bpa_cartesian: scratch allocation failed");
+        arrivals = reinterpret_cast<int *>(reinterpret_cast<char *>(part) + tiles * split * slab);
+        cudaMemsetAsync(arrivals, 0, tiles * sizeof(int), a.s);
+    }
     bpa_tile_kernel<VX, MINB, PAIR><<<(unsigned)(tiles * split), TL_THREADS, 0, a.s>>>(
         a.origin[0], a.origin[1], a.origin[2], a.step[0], a.step[1], a.step[2], a.nx, a.ny, a.nz,
-        a.vb, a.ve, a.el, a.m, a.env, a.k, a.out, a.oow, tx0, (int)tiles, split, part, a.rot);
-    if (split > 1) {
-        add_parts_kernel<<<4 * sm_count(), 256, 0, a.s>>>(a.out, part, split - 1, nv);
-        cudaFreeAsync(part, a.s);
-    }
+        a.vb, a.ve, a.el, a.m, a.env, a.k, a.out, a.oow, tx0, (int)tiles, split, part, arrivals,
+        a.rot);
+    if (part) cudaFreeAsync(part, a.s);
     return check_launch("bpa_tile_kernel");
 }
 
