@@ -130,7 +130,7 @@ class CubeUpload:
     pinned staging buffers (host copy of chunk i+1 overlaps the DMA of
     chunk i)."""
 
-    def __init__(self, values, device="cuda", rows=None, chunk_bytes: int = UPLOAD_CHUNK_BYTES):
+    def __init__(self, values, device="cuda", rows=None, chunk_bytes: int | None = None):
         import torch
         dev = torch.device(device)
         if dev.index is None:
@@ -144,7 +144,7 @@ class CubeUpload:
         self.h2d_bytes = (r1 - r0) * n_f * 8
         if r1 == r0:
             return
-        step = max(1, int(chunk_bytes // (n_f * 8)))
+        step = max(1, int((chunk_bytes or UPLOAD_CHUNK_BYTES) // (n_f * 8)))
         cs = copy_stream(dev)
         cs.wait_stream(torch.cuda.current_stream(dev))  # the destination is allocated
         pinned = host.is_pinned() and host.dtype == torch.complex64
