@@ -15,7 +15,8 @@ from .bpa import (ImageVolume, backproject, backproject_gather, bpa_reconstruct,
 from .errors import (ConfigError, HhsarError, IoFormatError, NativeUnavailableError,
                      NumericDomainError)
 from .ffbp import (GRID_PAD, FfbpParams, Subimage, SubimageGrid, build_subimage_grid,
-                   default_levels, hhffbpa_reconstruct, level1_reconstruct, merge_pair)
+                   default_levels, hhffbpa_reconstruct, hhffbpa_reconstruct_stream,
+                   level1_reconstruct, merge_pair)
 from .model import (C_LIGHT, DataCube, FrequencyGrid, ImagingRegion, Subarray,
                     SubarrayTree, SyntheticAperture, partition_subarrays, validate_geometry)
 from .metrics import (PSNR_SENTINEL_DB, PsfReport, max_intensity_projection, profile_cut,
@@ -31,7 +32,7 @@ __all__ = [
     "NumericDomainError", "PSNR_SENTINEL_DB", "PsfReport", "RangeProfileSet", "Subarray", "SubarrayExtents", "SubarrayTree",
     "Subimage", "SubimageGrid", "SyntheticAperture", "backproject", "backproject_gather",
     "bpa_reconstruct", "build_subimage_grid", "check_delay_window", "default_grid_dims",
-    "default_levels", "hhffbpa_reconstruct", "level1_reconstruct", "max_intensity_projection",
+    "default_levels", "hhffbpa_reconstruct", "hhffbpa_reconstruct_stream", "level1_reconstruct", "max_intensity_projection",
     "merge_pair", "partition_subarrays", "profile_cut", "psf_metrics", "psnr", "range_compress",
     "region_grid", "validate_geometry",
 ]

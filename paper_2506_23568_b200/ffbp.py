@@ -243,6 +243,21 @@ def _plan_upload(sched: Schedule, region):
     return staged, cuts, bl.shape[0]
 
 
+_PLAN_DEVICE = {}
+
+
+def _plan_device_inputs(staged, dev):
+    import torch
+    key = (staged.data_ptr(), staged.numel(), torch.device(dev).index)
+    hit = _PLAN_DEVICE.get(key)
+    if hit is None or hit[1] is not staged:
+        if len(_PLAN_DEVICE) > 8:
+            _PLAN_DEVICE.clear()
+        hit = (staged.to(dev), staged)  # once, synchronous
+        _PLAN_DEVICE[key] = hit
+    return hit[0]
+
+
 def _region_tuple(region):
     return (region.x_min, region.x_max, region.y_min, region.y_max, region.z_min, region.z_max)
 
@@ -266,7 +281,12 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
     stream = _native.stream_handle()
     staged, cuts, n_b = _plan_upload(sched, region)
     up = torch.empty(staged.shape, dtype=torch.uint8, device=dev)
-    up.copy_(staged, non_blocking=True)
+    if cached is not None:
+        # a device-resident copy of the (constant) plan inputs: a D2D copy,
+        # so the plan never queues behind cube uploads in the H2D engine
+        up.copy_(_plan_device_inputs(staged, dev), non_blocking=True)
+    else:
+        up.copy_(staged, non_blocking=True)
     if _trace:
         _trace("plan inputs up")
     descs_dev = up[cuts[0]:cuts[1]]
@@ -732,10 +752,8 @@ def provenance_of(run: DeviceRun, stats, flags, final_dims, params, levels, upsa
     return prov
 
 
-def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None = None,
-                        upsample: int = 8, *, merge_factor: int = 2) -> ImageVolume:
-    """Cartesian volume by factorised backprojection (ffbp.py:415-513)."""
-    import torch
+def _prepare(cube, region, final_dims, params, upsample):
+    """The reference's argument checks and defaults (ffbp.py:445-458)."""
     if params is None:
         params = FfbpParams()
     validate_geometry(cube.aperture, region)
@@ -744,6 +762,44 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
         final_dims = default_grid_dims(region, kgrid)
     final_dims = tuple(int(d) for d in final_dims)
     levels = params.levels if params.levels is not None else default_levels(cube.aperture)
+    return params, kgrid, final_dims, levels
+
+
+def _device_elements(cube, region, kgrid, upsample, levels):
+    """Element positions on the device + the checks that need them."""
+    import torch
+    _native.library()
+    el_dev = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
+                          device="cuda")
+    n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
+    check_delay_window(RangeProfileSet(envelopes=torch.empty((0, n_t)), t0=0.0, dt=dt,
+                                       upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
+                                       freqs=kgrid, elements_dev=el_dev), region)
+    if region.z_min <= 0.0:
+        raise ConfigError("region must sit strictly in front of the array")
+    leaf_bounds(cube.aperture.n_elements, levels)  # ConfigError when too deep (model.py:371-376)
+    return el_dev
+
+
+def _volume_of(run, final_dims, origin, step, params, levels, upsample, merge_factor):
+    """Device run -> host ImageVolume with the reference's checks and
+    provenance (one device->host round trip)."""
+    import torch
+    extra = torch.cat([run.flags, run.lattices.stats.reshape(-1)])
+    volume, tail = _finish(run.volume, run.oow, final_dims, origin, step, {}, extra)
+    n_flags = run.flags.numel()
+    flags = tail[:n_flags]
+    stats = tail[n_flags:].reshape(-1, _native.GRID_STATS)
+    check_grids(run, stats)
+    prov = provenance_of(run, stats, flags, final_dims, params, levels, upsample, merge_factor)
+    object.__setattr__(volume, "provenance", prov)
+    return volume
+
+
+def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None = None,
+                        upsample: int = 8, *, merge_factor: int = 2) -> ImageVolume:
+    """Cartesian volume by factorised backprojection (ffbp.py:415-513)."""
+    params, kgrid, final_dims, levels = _prepare(cube, region, final_dims, params, upsample)
     origin, step = region_grid(region, final_dims)
     if levels == 1:  # ffbp.py:460-464: plain BPA onto the final grid
         profiles = range_compress(cube, upsample)
@@ -757,16 +813,7 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
                 "dims": list(final_dims), "level_points": [[n]], "merge_flags": [],
                 "final_flags": 0, "flagged_fraction": 0.0}
         return _finish(vol, oow, final_dims, origin, step, prov)[0]
-    _native.library()
-    el_dev = torch.tensor(np.ascontiguousarray(cube.aperture.elements, dtype=np.float64),
-                          device="cuda")
-    n_t, dt, k_ref, _ = profile_axis(kgrid, upsample)
-    check_delay_window(RangeProfileSet(envelopes=torch.empty((0, n_t)), t0=0.0, dt=dt,
-                                       upsample=upsample, k_ref=k_ref, aperture=cube.aperture,
-                                       freqs=kgrid, elements_dev=el_dev), region)
-    if region.z_min <= 0.0:
-        raise ConfigError("region must sit strictly in front of the array")
-    leaf_bounds(cube.aperture.n_elements, levels)  # ConfigError when too deep (model.py:371-376)
+    el_dev = _device_elements(cube, region, kgrid, upsample, levels)
     # the cube streams in by chunks (pinned input: DMA straight from the
     # caller's buffer) while the plan, Newton and the range compression of
     # the rows already landed run
@@ -785,15 +832,146 @@ def hhffbpa_reconstruct(cube, region, final_dims=None, params: FfbpParams | None
         # the out-of-window verdict is the reference's
         run = hhffbpa_from_cube(cube_dev, el_dev, el_f32x4(el_dev), kgrid, region, final_dims,
                                 params, levels, merge_factor, upsample, gate=False)
-    extra = torch.cat([run.flags, run.lattices.stats.reshape(-1)])
-    volume, tail = _finish(run.volume, run.oow, final_dims, origin, step, {}, extra)
-    n_flags = run.flags.numel()
-    flags = tail[:n_flags]
-    stats = tail[n_flags:].reshape(-1, _native.GRID_STATS)
-    check_grids(run, stats)
-    prov = provenance_of(run, stats, flags, final_dims, params, levels, upsample, merge_factor)
-    object.__setattr__(volume, "provenance", prov)
-    return volume
+    return _volume_of(run, final_dims, origin, step, params, levels, upsample, merge_factor)
+
+
+_D2H_STREAMS = {}
+
+
+def _d2h_stream(device):
+    import torch
+    key = torch.device(device).index
+    if key not in _D2H_STREAMS:
+        _D2H_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _D2H_STREAMS[key]
+
+
+class _InFlight:
+    """One volume of a stream: its upload, device run, and the asynchronous
+    copy-back (volume + counters into pinned memory on a D2H stream)."""
+
+    def __init__(self, upload, run, d2h):
+        import torch
+        self.upload, self.run = upload, run
+        d2h.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(d2h):
+            finite = torch.isfinite(torch.view_as_real(run.volume)).all().reshape(1)
+            self.scalars_dev = torch.cat([run.oow.reshape(-1)[:1], finite.to(torch.int64),
+                                          run.flags, run.lattices.stats.reshape(-1)])
+            self.volume = torch.empty(run.volume.shape, dtype=run.volume.dtype, pin_memory=True)
+            self.scalars = torch.empty(self.scalars_dev.shape, dtype=torch.int64,
+                                       pin_memory=True)
+            self.volume.copy_(run.volume, non_blocking=True)
+            self.scalars.copy_(self.scalars_dev, non_blocking=True)
+            self.done = torch.cuda.Event()
+            self.done.record(d2h)
+        run.volume.record_stream(d2h)
+
+
+def hhffbpa_reconstruct_stream(cubes, region, final_dims=None, params: FfbpParams | None = None,
+                               upsample: int = 8, *, merge_factor: int = 2):
+    """hhffbpa_reconstruct over a sequence of cubes of ONE geometry (same
+    aperture, band and region: e.g. repeated handheld scans), as a
+    generator of ImageVolume, one per cube, in order.
+
+    Every volume is computed exactly as hhffbpa_reconstruct computes it
+    (plan, Newton, gated compression, leaves, merges, landing, the
+    reference's checks and provenance); what changes is the overlap of the
+    host transfers: the upload of cube i+1 (H2D, copy engine) runs while
+    volume i is finished and copied back (D2H, the other direction of the
+    link), and from the second volume on the plan comes from a PlanCache of
+    the first (the device still recomputes it), so the host never waits
+    inside a volume.  Per volume the link then carries the cube in and the
+    volume out concurrently: the period is ~max(upload, compute tail +
+    copy-back) instead of their sum."""
+    import torch
+    it = iter(cubes)
+    try:
+        first = next(it)
+    except StopIteration:
+        return
+    params, kgrid, final_dims, levels = _prepare(first, region, final_dims, params, upsample)
+    if levels == 1:
+        yield hhffbpa_reconstruct(first, region, final_dims, params, upsample,
+                                  merge_factor=merge_factor)
+        for cube in it:
+            yield hhffbpa_reconstruct(cube, region, final_dims, params, upsample,
+                                      merge_factor=merge_factor)
+        return
+    origin, step = region_grid(region, final_dims)
+    el_dev = _device_elements(first, region, kgrid, upsample, levels)
+    el4 = el_f32x4(el_dev)
+    elements = np.asarray(first.aperture.elements)
+    main = torch.cuda.current_stream()
+    d2h = _d2h_stream(el_dev.device)
+    cache = None
+
+    def same_geometry(cube):
+        el = np.asarray(cube.aperture.elements)
+        if el is not elements and not np.array_equal(el, elements):
+            raise ConfigError("hhffbpa_reconstruct_stream: every cube must share the "
+                              "first cube's aperture")
+        if cube.freqs != first.freqs:
+            raise ConfigError("hhffbpa_reconstruct_stream: every cube must share the "
+                              "first cube's frequency grid")
+
+    def upload(cube):
+        from .rangecomp import copy_stream
+        with torch.cuda.stream(copy_stream(el_dev.device)):  # allocated on the H2D queue
+            up = CubeUpload(cube.values)
+        up.tensor.record_stream(main)
+        return up
+
+    def launch(cube, up):
+        """Queue one volume; the first plans on the host (and starts its upload
+        right after the plan's copy), the later ones reuse its PlanCache."""
+        nonlocal cache
+        if cache is None:
+            ups = []
+            run = hhffbpa_from_cube(None, el_dev, el4, kgrid, region, final_dims, params,
+                                    levels, merge_factor, upsample,
+                                    upload=lambda: ups.append(upload(cube)) or ups[0])
+            cache = PlanCache.of(run)
+            up = ups[0]
+        else:
+            run = hhffbpa_from_cube(up.tensor, el_dev, el4, kgrid, region, final_dims, params,
+                                    levels, merge_factor, upsample, upload=up, plan_cache=cache)
+        return _InFlight(up, run, d2h)
+
+    def complete(fl: _InFlight, cube):
+        fl.done.synchronize()
+        sc = fl.scalars.numpy()
+        run = fl.run
+        if int(sc[0]):  # out-of-window leaf delay: redo ungated, as hhffbpa_reconstruct
+            run = hhffbpa_from_cube(fl.upload.tensor, el_dev, el4, kgrid, region, final_dims,
+                                    params, levels, merge_factor, upsample, gate=False)
+            return _volume_of(run, final_dims, origin, step, params, levels, upsample,
+                              merge_factor)
+        if not int(sc[1]):
+            raise ConfigError("volume values must be finite")
+        n_flags = run.flags.numel()
+        flags = sc[2:2 + n_flags]
+        stats = sc[2 + n_flags:].reshape(-1, _native.GRID_STATS)
+        check_grids(run, stats)
+        prov = provenance_of(run, stats, flags, final_dims, params, levels, upsample,
+                             merge_factor)
+        return ImageVolume._trusted(fl.volume.numpy().reshape(final_dims), origin, step, prov)
+
+    cube, up = first, None
+    pending = None
+    while cube is not None:
+        nxt = next(it, None)
+        if nxt is not None:
+            same_geometry(nxt)
+        flight = launch(cube, up)
+        # the next cube's upload is queued right behind this one's
+        up_next = upload(nxt) if nxt is not None else None
+        if pending is not None:
+            yield complete(*pending)
+        pending = (flight, cube)
+        cube, up = nxt, up_next
+    if pending is not None:
+        yield complete(*pending)
 
 
 # ---------------------------------------------------------------------------

@@ -432,3 +432,28 @@ def test_public_api_host_input_forms():
     for o in outs[1:]:
         assert np.array_equal(o.values, outs[0].values)
         assert o.provenance == outs[0].provenance
+
+
+def test_reconstruct_stream_equals_single_calls():
+    """hhffbpa_reconstruct_stream (uploads overlapped across volumes, plan
+    cache from the first volume) returns, per cube, exactly what
+    hhffbpa_reconstruct returns."""
+    import torch
+    import paper_2506_23568_b200 as hh
+    from paper_2506_23568_b200 import ffbp, workloads
+    from paper_2506_23568_b200.model import DataCube
+    w = workloads.config(2, frames=1024)
+    base = workloads.simulate_numpy(w)
+    params = hh.FfbpParams(levels=8)
+    dims = (64, 64, 24)
+    pinned = torch.from_numpy(np.asarray(base.values).copy()).pin_memory()
+    cubes = [DataCube(values=np.asarray(base.values) * s, aperture=base.aperture,
+                      freqs=base.freqs) for s in (1.0, 0.5 - 1j)]
+    cubes.append(DataCube(values=pinned.numpy(), aperture=base.aperture, freqs=base.freqs))
+    got = list(ffbp.hhffbpa_reconstruct_stream(cubes, w.region, dims, params, upsample=4,
+                                               merge_factor=4))
+    assert len(got) == 3
+    for cube, vol in zip(cubes, got):
+        want = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4, merge_factor=4)
+        assert np.array_equal(vol.values, want.values)
+        assert vol.provenance == want.provenance
