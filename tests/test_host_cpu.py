@@ -234,3 +234,35 @@ def test_leaf_range_gate_host_restatement():
     # clipped at the profile end
     b0c, wc = ffbp.leaf_range_gate(lat, sched, dt, want_b1 - 5)
     assert b0c == want_b0 and b0c + wc == want_b1 - 5
+
+
+def test_check_grids_reference_order():
+    """The vectorised SubimageGrid health check raises for the FIRST failing
+    grid in the reference's order -- each leaf as built, then after its
+    delay mask (ffbp.py:331-335), then the parents level by level -- with
+    the reference's message (ffbp.py:127-133)."""
+    from types import SimpleNamespace
+    from paper_2506_23568_b200 import _native, ffbp
+    from paper_2506_23568_b200.errors import NumericDomainError
+    sched = ffbp.Schedule(64, 4)  # 8 leaves, 4 + 2 parents
+    d = np.zeros(sched.n_grids, dtype=_native.GRID_DTYPE)
+    d["core_lo"] = 0
+    d["core_hi"] = 9  # 10 x 10 x 10 = 1,000 core points per grid
+    run = SimpleNamespace(sched=sched, lattices=SimpleNamespace(descs=d))
+    stats = np.zeros((sched.n_grids, _native.GRID_STATS), dtype=np.int64)
+    stats[:, 1] = stats[:, 3] = 1000
+    ffbp.check_grids(run, stats)  # healthy: no raise
+    s2 = stats.copy()
+    s2[3, 3] = 400   # leaf 3 after its delay mask: 60% masked
+    s2[9, 1] = 100   # a parent: 90% masked -- later in the reference's order
+    with pytest.raises(NumericDomainError, match="60% of core lattice points"):
+        ffbp.check_grids(run, s2)
+    s3 = stats.copy()
+    s3[5, 1] = 490   # leaf 5 as built: 51% masked beats leaf 6's masked state
+    s3[6, 3] = 0
+    with pytest.raises(NumericDomainError, match="51% of core lattice points"):
+        ffbp.check_grids(run, s3)
+    s4 = stats.copy()
+    s4[sched.level_slices[1][0] + 1, 1] = 500  # exactly 50%: the reference raises at >= 0.5
+    with pytest.raises(NumericDomainError, match="50% of core lattice points"):
+        ffbp.check_grids(run, s4)
