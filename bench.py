@@ -264,12 +264,17 @@ def _timed_steps(step, steps, warmup, barrier=None):
     return total / steps, per, out
 
 
+def _coll_device():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def _max_over_ranks(vals, world):
     if world == 1:
         return vals
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    t = torch.tensor(vals, dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(v) for v in t.cpu()]
 
@@ -300,9 +305,17 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = _dist_env()
+    # debug mode (HHSAR_BENCH_SHARED_GPU=1): every rank on cuda:0 over gloo
+    # (host-staged collectives, so no kernel waits on another rank) -- runs
+    # the N-rank code path on a one-GPU box; never a scaling measurement
+    shared = os.environ.get("HHSAR_BENCH_SHARED_GPU") == "1"
     if world > 1:
+        local = 0 if shared else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     from paper_2506_23568_b200 import _native, bpa, dist as hdist, ffbp, workloads
@@ -382,7 +395,9 @@ def run_ours(args):
                     "1,024 f -> 4,096 bins, 1024x1024x256, factor 4, M=12",
         "units_per_step": w.bpa_units,
         "grids": int(sched.n_grids),
-        "parallelism": f"subaperture groups + voxel slabs x{world}" if world > 1 else "1 GPU",
+        "parallelism": (f"subaperture groups + voxel slabs x{world}" +
+                        (" (debug: ranks share one GPU over gloo)" if shared else ""))
+                       if world > 1 else "1 GPU",
         "output": "voxel-sharded (each rank its slab)" if world > 1 else "device volume",
         "step": "CUDA-graph replay, all stages" if world == 1 else "per-rank sharded step",
         "l2": "inputs > L2 (17.2 GB cube per step)"}
@@ -504,7 +519,7 @@ def e2e_leg(args, w, params, cube, e0, e1, world, rank, dev):
     h2d = int(host.numel() * 8 + w.n_elements * 3 * 8)
     d2h = int((ve - vb) * 8)
     if world > 1:
-        t = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
+        t = torch.tensor([h2d, d2h], dtype=torch.int64, device=_coll_device())
         dist.all_reduce(t)
         h2d, d2h = int(t[0]), int(t[1])
     e2e = {"value": round(w.bpa_units / med / 1e9, 1), "unit": UNIT,

@@ -92,22 +92,32 @@ def bpa_reconstruct_sharded(cube, region, dims=None, upsample: int = 8, group=No
 # ---------------------------------------------------------------------------
 
 class TorchComm:
-    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """Collectives over torch.distributed: NCCL on GPUs; with a host backend
+    (gloo) device tensors are staged through host memory -- the CPU tests'
+    and a debug mode's path (several ranks sharing one GPU, where no kernel
+    may wait on another rank)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.host_stage = dist.is_initialized() and dist.get_backend(group) != "nccl"
 
     def _raw(self, t):
         import torch
         return torch.view_as_real(t) if t.is_complex() else t
 
+    def _host(self, t):
+        return t.cpu() if self.host_stage and t.is_cuda else t
+
     def allreduce_sum(self, t) -> None:
         import torch.distributed as dist
         if self.world > 1:
-            dist.all_reduce(t, group=self.group)
+            h = self._host(t)
+            dist.all_reduce(h, group=self.group)
+            if h is not t:
+                t.copy_(h)
 
     def allgather_segments(self, buf, segments) -> None:
         """buf[a_r:b_r] holds rank r's data on rank r; afterwards every rank
@@ -120,11 +130,12 @@ class TorchComm:
         a, b = segments[self.rank]
         send = torch.zeros(longest, dtype=buf.dtype, device=buf.device)
         send[:b - a] = buf[a:b]
-        recv = torch.empty(longest * self.world, dtype=buf.dtype, device=buf.device)
+        send = self._host(send)
+        recv = torch.empty(longest * self.world, dtype=buf.dtype, device=send.device)
         dist.all_gather_into_tensor(self._raw(recv), self._raw(send), group=self.group)
         for r, (a, b) in enumerate(segments):
             if r != self.rank:
-                buf[a:b] = recv[r * longest: r * longest + (b - a)]
+                buf[a:b] = recv[r * longest: r * longest + (b - a)].to(buf.device)
 
     def gather_segments(self, buf, segments, root: int = 0, base: int = 0) -> None:
         """Like allgather_segments, but only ``root`` receives the other
@@ -139,14 +150,15 @@ class TorchComm:
         a, b = segments[self.rank]
         send = torch.zeros(longest, dtype=buf.dtype, device=buf.device)
         send[:b - a] = buf[a - base:b - base]
+        send = self._host(send)
         if self.rank == root:
-            parts = [torch.empty(longest, dtype=buf.dtype, device=buf.device)
+            parts = [torch.empty(longest, dtype=buf.dtype, device=send.device)
                      for _ in range(self.world)]
             dist.gather(self._raw(send), [self._raw(p) for p in parts], dst=root,
                         group=self.group)
             for r, (a, b) in enumerate(segments):
                 if r != self.rank:
-                    buf[a - base:b - base] = parts[r][:b - a]
+                    buf[a - base:b - base] = parts[r][:b - a].to(buf.device)
         else:
             dist.gather(self._raw(send), None, dst=root, group=self.group)
 
