@@ -680,10 +680,7 @@ def cpu_baseline_leg(w, rows_dev, args):
             host_rows[(a, b)] = rows_dev[a:b].cpu().numpy()
         return host_rows[(a, b)]
 
-    try:
-        hh = reference.load()
-    except ImportError as exc:
-        return {"value": None, "unit": UNIT, "kind": "unavailable", "reason": str(exc)}
+    hh, kind = reference.load_or_port()
     refarm.warm_jit(hh)
     s = refarm.Config4Reference(hh, w, rows_fn)
     s.prepare_upper()
@@ -692,7 +689,7 @@ def cpu_baseline_leg(w, rows_dev, args):
     s.fill()
     t = s.sample.volume_seconds()
     return {"value": round(w.bpa_units / t / 1e9, 3), "unit": UNIT, "cores": reference.threads(),
-            "kind": "reference",
+            "kind": kind,
             "sample": f"{steps} sampled subtree+merge+slice steps ({sum(wall):.1f} s), "
                       f"extrapolated to {t:.0f} s/volume (oracle/refarm.py)",
             "cpu": _cpu_model()}
@@ -784,6 +781,7 @@ def reference_leg_config3(out, held):
         same, gap = _peak_check(vol.values, vol_ref)
         out["reference_s"] = ref["s"]
         out["reference_cores"] = ref["cores"]
+        out["reference_kind"] = ref["kind"]
         out["vs_reference_rel_l2"] = float(f"{rel:.3e}")
         out["vs_reference_peak_equal"] = same
         out["vs_reference_level_points_equal"] = vol.provenance["level_points"] == ref["level_points"]
@@ -794,10 +792,7 @@ def reference_leg_config3(out, held):
 def reference_full_run(w, values):
     """hhsar.hhffbpa_reconstruct (the staged reference) on the whole cube."""
     from oracle import reference, refarm
-    try:
-        hh = reference.load()
-    except ImportError as exc:
-        return {"unavailable": str(exc)}, None
+    hh, kind = reference.load_or_port()
     refarm.warm_jit(hh)
     freqs, region = refarm._to_ref(hh, w)
     ap = hh.SyntheticAperture(elements=np.asarray(w.aperture.elements), nx=w.aperture.nx,
@@ -808,7 +803,7 @@ def reference_full_run(w, values):
                                  upsample=w.upsample)
     s = time.perf_counter() - t
     return {"s": round(s, 2), "value": round(w.bpa_units / s / 1e9, 3), "unit": UNIT,
-            "cores": reference.threads(), "kind": "reference",
+            "cores": reference.threads(), "kind": kind,
             "level_points": vol.provenance["level_points"]}, np.asarray(vol.values)
 
 
@@ -825,11 +820,7 @@ def run_reference(args):
     from paper_2506_23568_b200 import workloads
     from oracle import reference, refarm
     w = workloads.config(HEADLINE)
-    try:
-        hh = reference.load()
-        kind = "reference"
-    except ImportError as exc:
-        return {"impl": "reference", "unavailable": f"reference not staged: {exc}"}
+    hh, kind = reference.load_or_port()  # the oracle port only if oracle/_ref is missing
     rng = np.random.default_rng(w.seed)
     cache = {}
 

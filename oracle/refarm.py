@@ -216,7 +216,10 @@ class Config4Reference:
 
 def warm_jit(hh) -> None:
     """The reference's own JIT warm-up (cli.py:357-362): one tiny
-    reconstruction compiles every Numba kernel before anything is timed."""
+    reconstruction compiles every Numba kernel before anything is timed
+    (nothing to compile for the oracle port)."""
+    if getattr(hh, "PORT", False):
+        return
     ap = hh.SyntheticAperture(elements=np.column_stack([
         np.repeat(np.linspace(-0.01, 0.01, 4), 4), np.tile(np.linspace(-0.01, 0.01, 4), 4),
         np.zeros(16)]), nx=4, ny=4)

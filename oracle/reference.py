@@ -66,8 +66,21 @@ def load():
     return hhsar
 
 
+def load_or_port():
+    """(module, kind): the staged reference package ("reference") or, where
+    it is missing, the oracle port behind the same API (oracle/port_api.py,
+    "port")."""
+    try:
+        return load(), "reference"
+    except ImportError:
+        from . import pipeline, port_api
+        pipeline.build_library()
+        return port_api, "port"
+
+
 def threads() -> int:
-    """Numba's thread count (default: every host core)."""
+    """Numba's thread count (default: every host core); the port's OpenMP
+    loops use the same."""
     try:
         import numba
         return int(numba.get_num_threads())

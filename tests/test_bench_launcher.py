@@ -45,3 +45,19 @@ def test_launch_command_uses_loopback_and_n_ranks():
     assert cmd[1:3] == ["-m", "torch.distributed.run"]
     assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd and "29555" in cmd
     assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+
+
+def test_reference_arm_falls_back_to_the_oracle_port(monkeypatch, tmp_path):
+    """Without the staged reference (oracle/_ref), --impl reference still
+    times the same sampled config-4 pieces, through the oracle port, and
+    says so (cpu_baseline.kind == "port")."""
+    import bench
+    from oracle import reference
+    monkeypatch.setattr(reference, "REF_DIR", tmp_path / "absent")
+
+    class Args:
+        steps, warmup = 1, 0
+    res = bench.run_reference(Args)
+    assert res["impl"] == "reference" and res["cpu_baseline"]["kind"] == "port"
+    assert res["value"] > 0 and res["e2e"]["value"] == res["value"]
+    assert res["higher_is_better"] is True and res["unit"] == bench.UNIT
