@@ -292,6 +292,7 @@ grid_plan_kernel(hhsar_grid_desc *__restrict__ grids, const double *__restrict__
 constexpr int NEWTON_THREADS = 128;
 constexpr int HEAVY_MAXP = 64;  // planes per heavy column held in shared memory
 constexpr int64_t NEWTON_SPEC2_MAX_COLS = 131072;  // speculative continuations up to this size
+constexpr int SPEC_DEPTH = 8;  // warm planes a speculative chain runs past its centre start
 
 __device__ __forceinline__ int grid_of_column(const hhsar_grid_desc *__restrict__ grids,
                                               int n_grids, const int32_t *__restrict__ block_grid,
@@ -487,12 +488,13 @@ __global__ void grid_newton_heavy_list_kernel(const hhsar_grid_desc *__restrict_
     if (h) heavy[b0 + __popc(m & ((1u << lane) - 1u))] = (int32_t)c;
 }
 
-// SPEC2 (heavy phase, small problems): a heavy plane whose centre start
-// converged goes on to solve the NEXT plane warm-started from it and stores
-// that in spec2_* (slot [heavy index][plane]) -- exactly the solve the fix-up
-// would run when that centre-started plane is the one the reference
-// converged on, so the fix-up's chain shrinks to runs of >= 2 converged
-// planes.
+// SPEC2 (heavy phase, small problems): a heavy plane s whose centre start
+// converged goes on warm through the next planes -- s+1 from s, s+2 from
+// s+1, ... while they converge, up to SPEC_DEPTH planes -- and stores plane
+// s+d in spec2_* slot [heavy index][plane s+d][d-1].  When the reference's
+// run of converged planes starts at s (s-1 failed, so s itself started
+// from the centre), that chain IS the reference's sequence of solves, so
+// the in-order fix-up only solves planes deeper than SPEC_DEPTH into a run.
 template <bool SPEC2>
 __global__ void __launch_bounds__(NEWTON_THREADS)
 grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64_t n_cols,
@@ -507,6 +509,7 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
     int64_t base = 0;  // lattice index of plane 0 of the current column
     bool have = false, core_uv = false, spec = false, warm2 = false;
     int64_t hslot = 0;  // SPEC2: heavy index * HEAVY_MAXP
+    int depth = 0;      // SPEC2: warm planes past the centre start
     double tu = 0, tv = 0, tn = 0, x = 0, y = 0, z = 0;
     const double max_step2 = g.max_step * g.max_step;
     // phase 0: heavy (column, plane) slots only; phase 1: light columns only
@@ -540,8 +543,10 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
                 if constexpr (SPEC2) {
                     hslot = (int64_t)(t / HEAVY_MAXP) * HEAVY_MAXP;
                     warm2 = false;
-                    // the warm continuation needs the next plane and a slot
-                    if (w + 1 < wend_col && (int64_t)(t / HEAVY_MAXP) < spec2_cap) w_end = w + 2;
+                    depth = 0;
+                    // the warm continuation needs the next planes and a slot
+                    if (w + 1 < wend_col && (int64_t)(t / HEAVY_MAXP) < spec2_cap)
+                        w_end = min(wend_col, w + 1 + SPEC_DEPTH);
                 }
             } else {
                 w = 0;
@@ -573,11 +578,18 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
         const bool ok = st == 1;
         if (spec) {  // speculative: the fix-up kernel decides
             if (SPEC2 && warm2) {
-                spec2_code[hslot + w] = spec_code(ok, it);
-                double *pp = spec2_pos + 3 * (hslot + w);
+                const int64_t slot = (hslot + w) * SPEC_DEPTH + (depth - 1);
+                spec2_code[slot] = spec_code(ok, it);
+                double *pp = spec2_pos + 3 * slot;
                 pp[0] = x;
                 pp[1] = y;
                 pp[2] = z;
+                if (ok && w + 1 < w_end) {  // the chain goes on
+                    ++w;
+                    ++depth;
+                    start_plane(D, x, y, z);
+                    continue;
+                }
                 have = false;
                 continue;
             }
@@ -586,8 +598,9 @@ grid_newton_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids, int64
             pp[0] = x;
             pp[1] = y;
             pp[2] = z;
-            if (SPEC2 && ok && w + 1 < w_end) {  // continue warm on the next plane
+            if (SPEC2 && ok && w + 1 < w_end) {  // continue warm on the next planes
                 warm2 = true;
+                depth = 1;
                 ++w;
                 start_plane(D, x, y, z);
                 continue;
@@ -632,7 +645,8 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
     const bool core_uv = q.iu >= D.core_lo[0] && q.iu <= D.core_hi[0] && q.iv >= D.core_lo[1] &&
                          q.iv <= D.core_hi[1];
     unsigned acc[6] = {0, 0, 0, 0, 0, 0};
-    bool prev_ok = false, prev_cold = true;
+    bool prev_ok = false;
+    int run_start = 0;  // the plane the current run of converged planes started at
     double px = 0, py = 0, pz = 0;
     const bool has2 = spec2_code != nullptr && i < spec2_cap;
     for (int w = 0; w < w_end; ++w) {
@@ -642,7 +656,10 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
         int it;
         double x, y, z;
         const bool cold = !prev_ok;
-        const uint8_t code2 = (has2 && !cold && prev_cold) ? spec2_code[i * HEAVY_MAXP + w] : 0xff;
+        if (cold) run_start = w;
+        const int depth = w - run_start;  // warm planes past the run's centre start
+        const int64_t slot = ((int64_t)i * HEAVY_MAXP + w) * SPEC_DEPTH + (depth - 1);
+        const uint8_t code2 = (has2 && !cold && depth <= SPEC_DEPTH) ? spec2_code[slot] : 0xff;
         if (cold) {  // the reference also started this plane from the centre
             ok = code & 0x80;
             it = code & 0x7f;
@@ -650,11 +667,11 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
             y = pp[1];
             z = pp[2];
         } else if (code2 != 0xff) {
-            // predecessor = its centre start, whose warm continuation the
-            // heavy phase already solved
+            // the heavy phase's chain from this run's centre start already
+            // solved this plane exactly as the reference does
             ok = code2 & 0x80;
             it = code2 & 0x7f;
-            const double *q = spec2_pos + 3 * (i * HEAVY_MAXP + w);
+            const double *q = spec2_pos + 3 * slot;
             x = q[0];
             y = q[1];
             z = q[2];
@@ -669,7 +686,6 @@ grid_newton_fixup_kernel(const hhsar_grid_desc *__restrict__ grids, int n_grids,
         acc[5] += 1;
         finish_plane(D, g, w, ok, x, y, z, core_uv, base, valid, positions, acc);
         prev_ok = ok;
-        prev_cold = cold;
         px = x;
         py = y;
         pz = z;
@@ -894,7 +910,7 @@ extern "C" int hhsar_grid_newton(const hhsar_grid_desc *grids, int64_t n_grids, 
     // the column -> grid map, and (SPEC2) the continuation slots
     unsigned long long *counter = nullptr;
     const size_t head = 2 * sizeof(unsigned long long) + 2 * n_cols * sizeof(int32_t);
-    const size_t slots = (size_t)cap * HEAVY_MAXP;
+    const size_t slots = (size_t)cap * HEAVY_MAXP * SPEC_DEPTH;
     if (cudaMallocAsync(&counter, head + slots * (3 * sizeof(double) + 1), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "grid_newton: scratch allocation failed");
     cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), s);
