@@ -457,3 +457,22 @@ def test_reconstruct_stream_equals_single_calls():
         want = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4, merge_factor=4)
         assert np.array_equal(vol.values, want.values)
         assert vol.provenance == want.provenance
+
+
+@pytest.mark.parametrize("factor", [2, 4])
+def test_config0_hhffbpa_cubic_vs_oracle(hh, config0, factor):
+    """Keys-cubic interpolation (FfbpParams(kernel='cubic'), _kernels.py:155-200)
+    through the whole config-0 pipeline, binary and factor-4 schedules, against
+    the oracle (pinned to the reference's cubic goldens at small scale)."""
+    import oracle
+    vol = hh.hhffbpa_reconstruct(config0.cube, config0.region, config0.dims,
+                                 hh.FfbpParams(levels=7, kernel="cubic"), upsample=8,
+                                 merge_factor=factor)
+    want, _, _, prov = oracle.hhffbpa_reconstruct(config0.cube, config0.region, config0.dims,
+                                                  levels=7, kernel="cubic", upsample=8,
+                                                  merge_factor=factor)
+    err = assert_image_parity(vol.values, want)
+    assert vol.provenance["level_points"] == prov["level_points"]
+    assert vol.provenance["merge_flags"] == prov["merge_flags"]
+    assert vol.provenance["final_flags"] == prov["final_flags"]
+    print(f"config0 cubic factor {factor} rel-L2 {err:.2e}")
