@@ -476,3 +476,28 @@ def test_config0_hhffbpa_cubic_vs_oracle(hh, config0, factor):
     assert vol.provenance["merge_flags"] == prov["merge_flags"]
     assert vol.provenance["final_flags"] == prov["final_flags"]
     print(f"config0 cubic factor {factor} rel-L2 {err:.2e}")
+
+
+def test_sdc_phase_operator_vs_reference(hh, small):
+    """S1 at operator level: hhsar_downconvert on unit values returns
+    exp(-j Phi(pos)) with Phi the reference's sdc_phase (spectrum.py:229-240,
+    golden map_phase on 64 random region points); float64 phase, reduced
+    before the float32 sincos."""
+    import torch
+    from paper_2506_23568_b200 import _native, ffbp
+    z = small.z
+    pts = np.ascontiguousarray(z["map_points"], dtype=np.float64)
+    n = pts.shape[0]
+    e = z["newton_ext"]
+    desc = ffbp._one_desc(tuple(e), np.zeros(3), (n, 1, 1), 0, 0, 0)
+    d_dev = _native.device_struct(desc, torch.device("cuda"))
+    pos = torch.as_tensor(pts, device="cuda")
+    valid = torch.ones(n, dtype=torch.uint8, device="cuda")
+    vals = torch.ones(n, dtype=torch.complex64, device="cuda")
+    geom = ffbp._geom_for(small.freqs)
+    _native.call("hhsar_downconvert", _native.ptr(d_dev), 1, n, _native.ptr(pos),
+                 _native.ptr(valid), _native.ptr(geom), _native.ptr(vals),
+                 _native.stream_handle())
+    got = vals.cpu().numpy().astype(np.complex128)
+    want = np.exp(-1j * z["map_phase"])
+    assert np.max(np.abs(got - want)) < 2e-6
