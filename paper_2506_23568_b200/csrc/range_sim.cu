@@ -335,6 +335,171 @@ int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const
     return check_launch("range_compress_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Gated range compression of 4096-bin rows (BASELINE config 4: n_f = 1024
+// or 512 live samples, a window of a few hundred bins): one smem exchange
+// instead of the Stockham kernel's two.  With n = 64 n1 + n2 and
+// k = k1 + 64 k2,
+//     X[k] = sum_{n2 < 64} W^{n2 k} A_{n2}[k1],
+//     A_{n2}[k1] = sum_{n1 < NL} x[64 n1 + n2] W64^{n1 k1}
+// (W = e^{+2 pi i / 4096}).  Stage A: thread n2 forms its column's 64
+// outputs as four 16-point DFTs (k1 = 4 q + r: x[n1] W64^{n1 r} then DFT16
+// over n1), the live NL inputs pruned statically.  Stage B: thread t owns
+// the window bins k = b0 + t + 64 o (column k1 = k mod 64): per 16-row slice
+// of its column one 4-point DFT, then a 16-term Horner chain per bin (see
+// rc4096_bins) and the demodulation.  The bins of one warp are contiguous
+// (coalesced stores) and their count is warp-uniform when the window is a
+// multiple of 32 bins.  One 64-thread CTA per row, 6 per SM; per row 32 KB
+// of smem written and read once (the Stockham kernel moves 64 KB) and ~100k
+// FP32 lane operations (the Stockham kernel: ~118k).  Tried and dropped:
+// one Horner chain over all 64 column entries per bin (+40% FP32 work),
+// persistent CTAs prefetching the next row (cp.async staging: 5 CTAs per
+// SM; register prefetch: barrier stalls) -- both slower.
+// ---------------------------------------------------------------------------
+struct Rc64Roots {
+    float2 w[64], iw[64];  // e^{+2 pi i m / 64} and i times it (kernel parameter space)
+    float2 dstep[8];       // e^{j a dt 64 o}: demodulation of bin k + 64 o relative to bin k
+};
+
+constexpr int RC64_LD = 65;  // padded column stride: stage B's column reads are conflict-free
+
+// stage B for one thread with C bins k = kb + 64 o, kb = b0 + t, o < C
+// (those at or past b0 + w are computed and dropped -- only in the warp
+// holding the window's ragged end).  With n2 = 16 a + b (a < 4, b < 16):
+//     X[k] = sum_b z^b Z_b[o mod 4],  z = W^k,
+//     Z_b[s] = sum_a (A_{16a+b}[k1] W^{16 a kb}) i^{a s}
+// since W^{16 a k} = W^{16 a kb} i^{a o}: per b one 4-point DFT (three
+// twiddles tau_a = W^{16 a kb}, per-thread constants) feeds every bin's
+// 16-term Horner chain.  d0 = the demodulation of bin kb; the other bins
+// follow by the constant steps W^{64 o} = W64^o and e^{j a dt 64 o}.
+template <int C>
+__device__ __forceinline__ void rc4096_bins(const float2 *__restrict__ col, const Rc64Roots &roots,
+                                            float2 z0, float2 tau1, float2 tau2, float2 tau3,
+                                            float2 d0, float2 *__restrict__ dst, int t, int w) {
+    f2x z[C], iz[C], acc[C];
+#pragma unroll
+    for (int o = 0; o < C; ++o) {
+        const float2 zf = o == 0 ? z0 : cmul_p(z0, as_x(roots.w[o]), as_x(roots.iw[o]));
+        z[o] = as_x(zf);
+        iz[o] = pk2(-zf.y, zf.x);
+    }
+    const f2x t1 = as_x(tau1), it1 = pk2(-tau1.y, tau1.x);
+    const f2x t2 = as_x(tau2), it2 = pk2(-tau2.y, tau2.x);
+    const f2x t3 = as_x(tau3), it3 = pk2(-tau3.y, tau3.x);
+#pragma unroll
+    for (int b = 15; b >= 0; --b) {
+        float2 u[4] = {col[b], cmul_p(col[16 + b], t1, it1), cmul_p(col[32 + b], t2, it2),
+                       cmul_p(col[48 + b], t3, it3)};
+        idft<4, 4>(u);
+#pragma unroll
+        for (int o = 0; o < C; ++o)
+            acc[o] = b == 15 ? as_x(u[o & 3])
+                             : fma2(bc2(hi2(acc[o])), iz[o], fma2(bc2(lo2(acc[o])), z[o], as_x(u[o & 3])));
+    }
+#pragma unroll
+    for (int o = 0; o < C; ++o) {
+        const int i = t + 64 * o;
+        if (i >= w) break;
+        const float2 d = o == 0 ? d0 : cmul(d0, roots.dstep[o]);
+        __stcs(dst + i, cmul(as_f(acc[o]), d));
+    }
+}
+
+#ifndef RC4096_PREFETCH
+#define RC4096_PREFETCH 2048  // rows ahead (~2 waves of 6 x 148 CTAs)
+#endif
+#ifndef RC4096_MINB
+#define RC4096_MINB 6  // CTAs per SM: 6 x 33 KB of smem
+#endif
+template <int NL, int CMAX>
+__global__ void __launch_bounds__(64, RC4096_MINB)
+range_compress_4096_kernel(const float2 *__restrict__ cube, int64_t n_el, const float2 *__restrict__ wk,
+                           const float2 *__restrict__ demod,
+                           const __grid_constant__ Rc64Roots roots, float2 *__restrict__ out,
+                           int gate_b0, int gate_w) {
+    __shared__ float2 cols[64 * RC64_LD];
+    const int t = threadIdx.x;
+    const int64_t row = blockIdx.x;
+    const float2 *src = cube + row * (64 * NL);
+    float2 x[NL];
+#pragma unroll
+    for (int n1 = 0; n1 < NL; ++n1) x[n1] = __ldcs(src + 64 * n1 + t);
+    // pull a later CTA's row into L2 (one bulk prefetch)
+    if (t == 0 && row + RC4096_PREFETCH < n_el)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + RC4096_PREFETCH * (64 * NL)),
+                     "r"(64 * NL * 8) : "memory");
+    // stage B's per-thread constants (the same for every row: L1/L2 hits),
+    // fetched now so their latency hides behind stage A
+    const int kb = gate_b0 + t;
+    const float2 z0 = __ldg(wk + (kb & 4095)), d0 = __ldg(demod + (kb < 4096 ? kb : 4095));
+    const float2 tau1 = __ldg(wk + ((16 * kb) & 4095)), tau2 = __ldg(wk + ((32 * kb) & 4095)),
+                 tau3 = __ldg(wk + ((48 * kb) & 4095));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        float2 v[16];
+#pragma unroll
+        for (int n1 = 0; n1 < NL; ++n1)
+            v[n1] = (r == 0 || n1 == 0)
+                        ? x[n1]
+                        : cmul_p(x[n1], as_x(roots.w[n1 * r]), as_x(roots.iw[n1 * r]));
+        idft<16, NL>(v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) cols[(4 * q + r) * RC64_LD + t] = v[q];
+    }
+    __syncthreads();
+    // bins per thread, uniform over the warp (max over its lanes)
+    const int cw = (gate_w - (t & ~31) + 63) >> 6;
+    const float2 *col = cols + (kb & 63) * RC64_LD;
+    float2 *dst = out + row * gate_w;
+    if (cw == CMAX) {
+        rc4096_bins<CMAX>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
+    } else if constexpr (CMAX > 1) {
+        if (cw == CMAX - 1) rc4096_bins<CMAX - 1>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
+    }
+}
+
+// W^k = e^{+2 pi i k / 4096} from float64
+__global__ void rc_wk_kernel(float2 *__restrict__ wk) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4096) return;
+    double sn, cs;
+    sincospi((double)i / 2048.0, &sn, &cs);
+    wk[i] = make_float2((float)cs, (float)sn);
+}
+
+template <int NL, int C>
+int launch_rc4096_c(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
+                    const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
+    auto kern = range_compress_4096_kernel<NL, C>;
+    // smem-heavy (6 CTAs of 33 KB per SM): ask for the full carveout
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    for (int64_t r0 = 0; r0 < n_el; r0 += 2147483647ll) {
+        const int64_t nb = n_el - r0 < 2147483647ll ? n_el - r0 : 2147483647ll;
+        kern<<<(unsigned)nb, 64, 0, s>>>(cube + r0 * (64 * NL), n_el - r0, wk, demod, roots,
+                                         out + r0 * (int64_t)gate_w, gate_b0, gate_w);
+    }
+    return check_launch("range_compress_4096_kernel");
+}
+
+// bins per stage-B thread: C = ceil(w / 64) <= RC4096_MAX_C
+constexpr int RC4096_MAX_C = 8;
+
+template <int NL>
+int launch_rc4096(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
+                  const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
+    switch ((gate_w + 63) / 64) {
+        case 1: return launch_rc4096_c<NL, 1>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 2: return launch_rc4096_c<NL, 2>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 3: return launch_rc4096_c<NL, 3>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 4: return launch_rc4096_c<NL, 4>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 5: return launch_rc4096_c<NL, 5>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 6: return launch_rc4096_c<NL, 6>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        case 7: return launch_rc4096_c<NL, 7>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        default: return launch_rc4096_c<NL, 8>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+    }
+}
+
 template <int LOGN>
 int launch_rc_up(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const float2 *demod,
                  const RcDemodSteps &steps, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
@@ -491,8 +656,8 @@ extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64
     HHSAR_REQUIRE(b0 >= 0 && w >= 1 && b0 + w <= n_t, "range_compress: bad bin window");
     if (n_el == 0) return HHSAR_OK;
     cudaStream_t s = as_stream(stream);
-    float2 *tables = nullptr;  // twiddles [n_t], then demodulation phases [n_t]
-    if (cudaMallocAsync(&tables, 2 * n_t * sizeof(float2), s) != cudaSuccess)
+    float2 *tables = nullptr;  // twiddles [n_t], demodulation phases [n_t], W^k [n_t]
+    if (cudaMallocAsync(&tables, 3 * n_t * sizeof(float2), s) != cudaSuccess)
         return set_error(HHSAR_ECUDA, "range_compress: table allocation failed");
     float2 *demod_tab = tables + n_t;
     rc_tables_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(tables, demod_tab, (int)n_t,
@@ -500,6 +665,27 @@ extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64
     auto c = reinterpret_cast<const float2 *>(cube);
     auto o = reinterpret_cast<float2 *>(out);
     int rc = HHSAR_OK;
+#ifndef HHSAR_RC_STOCKHAM_ONLY
+    if (n_t == 4096 && (n_f == 1024 || n_f == 512) && w <= 64 * RC4096_MAX_C) {
+        float2 *wk = tables + 2 * n_t;
+        rc_wk_kernel<<<16, 256, 0, s>>>(wk);
+        Rc64Roots roots;
+        for (int m = 0; m < 64; ++m) {
+            const double ph = 2.0 * M_PI * (double)m / 64.0;
+            roots.w[m] = make_float2((float)cos(ph), (float)sin(ph));
+            roots.iw[m] = make_float2(-roots.w[m].y, roots.w[m].x);
+        }
+        for (int o = 0; o < 8; ++o) {  // e^{j a dt 64 o}, reduced like cis_reduced
+            const double rev = a * (dt * 64.0 * (double)o) / (2.0 * M_PI);
+            const double red = 2.0 * M_PI * (rev - nearbyint(rev));
+            roots.dstep[o] = make_float2((float)cos(red), (float)sin(red));
+        }
+        rc = n_f == 1024 ? launch_rc4096<16>(c, n_el, wk, demod_tab, roots, o, (int)b0, (int)w, s)
+                         : launch_rc4096<8>(c, n_el, wk, demod_tab, roots, o, (int)b0, (int)w, s);
+        cudaFreeAsync(tables, s);
+        return rc;
+    }
+#endif
     RcDemodSteps st;
     const double step = dt * (double)(n_t / 16);
     for (int r = 0; r < 16; ++r) {  // e^{j a dt r n_t / 16}, reduced like cis_reduced

@@ -328,7 +328,12 @@ def test_config3_full_scale_vs_oracle(hh):
                                                     (5, 1024, 4, 4000, 96), (3, 128, 8, 300, 211),
                                                     (4, 64, 4, 17, 239),
                                                     (2000, 1024, 4, 49, 288),   # config 4 rows, its gate
-                                                    (3000, 512, 4, 0, 352)])    # config 3 rows, its gate
+                                                    (3000, 512, 4, 0, 352),     # config 3 rows, its gate
+                                                    # 4096-bin rows, gated: the one-exchange kernel
+                                                    (300, 1024, 4, 0, 512), (300, 1024, 4, 3584, 512),
+                                                    (70, 1024, 4, 4095, 1), (70, 1024, 4, 63, 65),
+                                                    (70, 1024, 4, 1000, 449), (70, 512, 8, 49, 288),
+                                                    (70, 512, 8, 3000, 1096)])
 def test_range_compress_window_equals_full_slice(n_el, n_f, upsample, b0, w):
     """The range-gated compression (only bins [b0, b0 + w) computed in the
     last pass and stored) against the same bins of the full compression."""
