@@ -265,12 +265,17 @@ int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_p
 /* Final landing on the Cartesian region_grid voxels [nx][ny][nz] (z
  * fastest), all n_children children, no downconversion (ffbp.py:493-495).
  * Voxels [vox_begin, vox_end) of the flattened volume are written to
- * out[0 .. vox_end - vox_begin) (voxel sharding across GPUs). */
+ * out[0 .. vox_end - vox_begin) (voxel sharding across GPUs).  The
+ * children's lattices occupy pool points [span_begin, span_begin +
+ * span_points) of child_values; with span_points > 0 the landing stages a
+ * 16-byte (v[i], v[i+1]) pair copy of that span for its gathers
+ * (span_points = 0: gathers from child_values directly). */
 int hhsar_merge_cartesian(const double *origin, const double *step, const int64_t *dims,
                           int64_t vox_begin, int64_t vox_end,
                           const hhsar_grid_desc *child_grids, int64_t n_children,
-                          const void *child_values, const hhsar_geom *geom, int kernel,
-                          void *out, int64_t *flagged, void *stream);
+                          const void *child_values, int64_t span_begin, int64_t span_points,
+                          const hhsar_geom *geom, int kernel, void *out, int64_t *flagged,
+                          void *stream);
 
 /* ---- input synthesis ------------------------------------------------------ */
 

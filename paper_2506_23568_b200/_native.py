@@ -71,7 +71,8 @@ SIGNATURES = {
     "hhsar_merge_level": ([_P, _I64, _I64, _P, _P, _P, _I64, _I32, _P, _P, _I32, _I32, _P, _P,
                            _P], ctypes.c_int),
     "hhsar_downconvert": ([_P, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
-    "hhsar_merge_cartesian": ([_P, _P, _P, _I64, _I64, _P, _I64, _P, _P, _I32, _P, _P, _P],
+    "hhsar_merge_cartesian": ([_P, _P, _P, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I32, _P,
+                               _P, _P],
                               ctypes.c_int),
     "hhsar_simulate": ([_P, _I64, _P, _P, _I64, _P, _I64, _P, _P], ctypes.c_int),
     "hhsar_simulate_uniform": ([_P, _I64, _P, _P, _I64, _D, _D, _I64, _P, _P], ctypes.c_int),

@@ -112,34 +112,28 @@ __device__ __forceinline__ void split_d(double c, int hi, int &i, float &f) {
     }
 }
 
-// Lattice interpolation with the reference's hull rules (_kernels.py:117-189)
-// on float u, v and double n lattice coordinates.
+// The lattice gather of one sample at integer bases (iu, iv, iw) and
+// fractions (fu, fv, fn) (_kernels.py:117-189): trilinear as nested lerps,
+// or Keys cubic over the 4 x 4 x 4 neighbourhood.
 template <int KERNEL>
-__device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, const MergeChild &C,
-                                             float cu, float cv, double cn, float2 &out) {
-    out = make_float2(0.f, 0.f);
-    const int lo = KERNEL ? 1 : 0;
-    if (!(cu >= (float)lo && cu <= C.hu + 1.f && cv >= (float)lo && cv <= C.hv + 1.f &&
-          cn >= (double)lo && cn <= (double)(C.nn - 1 - lo)))
-        return false;
-    int iu, iv, iw;
-    float fu, fv, fn;
-    split_f(cu, C.hu, iu, fu);
-    split_f(cv, C.hv, iv, fv);
-    split_d(cn, C.nn - (KERNEL ? 3 : 2), iw, fn);
+__device__ __forceinline__ float2 gather_child(const float2 *__restrict__ vals, const MergeChild &C,
+                                               int iu, int iv, int iw, float fu, float fv, float fn) {
     const int su = C.nv * C.nn;  // lattices hold < 2^31 points (int32 dims product)
     const float2 *base = vals + C.offset;
     float2 acc = make_float2(0.f, 0.f);
     if (KERNEL == 0) {
         // trilinear as nested lerps along n, v, u on (re, im) pairs: one
-        // FADD2 + one FFMA2 per lerp, no weight products
-        const float2 *b = base + ((iu * C.nv + iv) * C.nn + iw);
+        // FADD2 + one FFMA2 per lerp, no weight products; row addresses from
+        // 32-bit lattice indices (one wide multiply-add each)
+        const unsigned i00 = (unsigned)((iu * C.nv + iv) * C.nn + iw);
+        const unsigned idx[2][2] = {{i00, i00 + (unsigned)C.nn},
+                                    {i00 + (unsigned)su, i00 + (unsigned)(su + C.nn)}};
         f2x r[2][2];
 #pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int bb = 0; bb < 2; ++bb) {
-                const float2 *row = b + a * su + bb * C.nn;
+                const float2 *row = base + idx[a][bb];
                 const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
                 const f2x x0 = pk2(v0.x, v0.y);
                 r[a][bb] = fma2(bc2(fn), sub2(pk2(v1.x, v1.y), x0), x0);
@@ -168,7 +162,81 @@ __device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, co
                 }
             }
     }
-    out = acc;
+    return acc;
+}
+
+// The same gather from the pair-staged copy of the child lattices: entry i
+// holds (v[i], v[i + 1]) in 16 B, so each lattice row of the stencil is one
+// 128-bit load (linear: 4 per sample instead of 8; cubic: 32 instead of 64).
+template <int KERNEL>
+__device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ pairs,
+                                                     const MergeChild &C, int iu, int iv, int iw,
+                                                     float fu, float fv, float fn) {
+    const int su = C.nv * C.nn;
+    const float4 *base = pairs + C.offset;
+    if (KERNEL == 0) {
+        const unsigned i00 = (unsigned)((iu * C.nv + iv) * C.nn + iw);
+        const unsigned idx[2][2] = {{i00, i00 + (unsigned)C.nn},
+                                    {i00 + (unsigned)su, i00 + (unsigned)(su + C.nn)}};
+        f2x r[2][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb) {
+                const float4 v = __ldg(base + idx[a][bb]);
+                const f2x x0 = pk2(v.x, v.y);
+                r[a][bb] = fma2(bc2(fn), sub2(pk2(v.z, v.w), x0), x0);
+            }
+        const f2x s0 = fma2(bc2(fv), sub2(r[0][1], r[0][0]), r[0][0]);
+        const f2x s1 = fma2(bc2(fv), sub2(r[1][1], r[1][0]), r[1][0]);
+        const f2x a2 = fma2(bc2(fu), sub2(s1, s0), s0);
+        return make_float2(lo2(a2), hi2(a2));
+    } else {
+        float wu[4], wv[4], wn[4];
+        keys_weights(fu, wu);
+        keys_weights(fv, wv);
+        keys_weights(fn, wn);
+        const float4 *b = base + (((iu - 1) * C.nv + (iv - 1)) * C.nn + (iw - 1));
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const float4 *row = b + a * su + bb * C.nn;
+                const float w = wu[a] * wv[bb];
+                const float4 p0 = __ldg(row), p1 = __ldg(row + 2);
+                acc.x = fmaf(p0.x, w * wn[0], fmaf(p0.z, w * wn[1], fmaf(p1.x, w * wn[2], fmaf(p1.z, w * wn[3], acc.x))));
+                acc.y = fmaf(p0.y, w * wn[0], fmaf(p0.w, w * wn[1], fmaf(p1.y, w * wn[2], fmaf(p1.w, w * wn[3], acc.y))));
+            }
+        return acc;
+    }
+}
+
+// pairs[i - begin] = (v[i], v[i + 1]) for the child lattices' pool span
+__global__ void pair_rows_kernel(const float2 *__restrict__ vals, int64_t begin, int64_t n,
+                                 float4 *__restrict__ pairs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float2 a = vals[begin + i], b = vals[begin + (i + 1 < n ? i + 1 : i)];
+    pairs[i] = make_float4(a.x, a.y, b.x, b.y);
+}
+
+// Lattice interpolation with the reference's hull rules (_kernels.py:117-189)
+// on float u, v and double n lattice coordinates.
+template <int KERNEL>
+__device__ __forceinline__ bool sample_child(const float2 *__restrict__ vals, const MergeChild &C,
+                                             float cu, float cv, double cn, float2 &out) {
+    out = make_float2(0.f, 0.f);
+    const int lo = KERNEL ? 1 : 0;
+    if (!(cu >= (float)lo && cu <= C.hu + 1.f && cv >= (float)lo && cv <= C.hv + 1.f &&
+          cn >= (double)lo && cn <= (double)(C.nn - 1 - lo)))
+        return false;
+    int iu, iv, iw;
+    float fu, fv, fn;
+    split_f(cu, C.hu, iu, fu);
+    split_f(cv, C.hv, iv, fv);
+    split_d(cn, C.nn - (KERNEL ? 3 : 2), iw, fn);
+    out = gather_child<KERNEL>(vals, C, iu, iv, iw, fu, fv, fn);
     return true;
 }
 
@@ -342,6 +410,194 @@ merge_cartesian_kernel(double ox, double oy, double oz, double sx, double sy, do
     warp_add(flagged, fl);
 }
 
+// Cartesian landing along z by Taylor series.  Per (column, child) the
+// quantities a voxel needs -- the u and v lattice coordinates, the n
+// coordinate and the phase 0.25 (k_max sq + k_min r) -- are smooth in z, so
+// a thread owning ZQ consecutive z voxels evaluates them once, with their
+// first four z-derivatives, at the block's centre z_c and then per voxel as
+// quartic polynomials in t = (z - z_c) / sz (|t| <= (ZQ - 1) / 2):
+// * r = sum of the four corner distances d_i = sqrt(s_i + z^2):
+//   d_i^(k)/k! from y_i = 1/d_i (float64: s_i y_i^3 / 2, -s_i z y_i^5 / 2,
+//   s_i (4 z^2 - s_i) y_i^7 / 8); sq = sqrt(r^2 - gap) by the series square
+//   root of r^2 - gap; n and the phase are linear in (r, sq);
+// * u = c_uv w_x (a_x + b_x) / (d_a + d_b) by the series reciprocal of the
+//   clamped-lateral distance sum (float32, as the per-voxel form).
+// Per voxel the n coordinate is an integer base per block plus a float32
+// polynomial, and the phase's float32 polynomial starts from the block's
+// float64-reduced phase, so no float64 and no square root or reciprocal
+// remain per voxel (the per-voxel form: five float64 square roots, four
+// fp32 square roots, two reciprocals).  Truncation (fifth order) is
+// (ZQ sz / 2d)^5-small: <= 3e-7 rad of phase at config 3 (ZQ = 8, d >= 0.2
+// m), 7e-11 at config 4; the launcher falls back to the per-voxel kernel
+// when the region's nearest z is not far enough from the aperture plane.
+template <int KERNEL, int ZQ>
+__global__ void __launch_bounds__(MERGE_THREADS)
+merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double sy, double sz,
+                              int ny, int nz, int64_t vb, int64_t ve, int64_t q0, int64_t nq,
+                              const MergeChild *__restrict__ kids, int nk,
+                              const float2 *__restrict__ kv, const float4 *__restrict__ kp,
+                              hhsar_geom g, float2 *__restrict__ out,
+                              int64_t *__restrict__ flagged) {
+    const int64_t qi = (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
+    if (qi >= nq) return;
+    const int nzq = (nz + ZQ - 1) / ZQ;
+    const int64_t Q = q0 + qi;           // global block: column (ix, iy), z block k
+    const int64_t row = Q / nzq;
+    const int k = (int)(Q - row * nzq);
+    const int iy = (int)(row % ny), ix = (int)(row / ny);
+    const double x = __dadd_rn(ox, __dmul_rn(sx, (double)ix));
+    const double y = __dadd_rn(oy, __dmul_rn(sy, (double)iy));
+    const float xf = (float)x, yf = (float)y;
+    const double inv_step = rcp_d(g.step);
+    const double zc = oz + sz * ((double)(k * ZQ) + 0.5 * (ZQ - 1));
+    const double zc2 = zc * zc;
+    const float zcf = (float)zc, zc2f = (float)zc2;
+    const double sz2 = sz * sz, sz3 = sz2 * sz, sz4 = sz2 * sz2;
+    const float szf = (float)sz, sz2f = szf * szf, sz3f = sz2f * szf, sz4f = sz2f * sz2f;
+    float2 acc[ZQ];
+    unsigned good = (1u << ZQ) - 1u;
+#pragma unroll
+    for (int j = 0; j < ZQ; ++j) acc[j] = make_float2(0.f, 0.f);
+    constexpr int lo = KERNEL ? 1 : 0;
+    for (int c = 0; c < nk; ++c) {
+        const MergeChild C = load_child(kids + c);
+        // ---- n coordinate and phase: float64 series of r and sq at z_c
+        const double ax = x - C.ext[0], bx = x - C.ext[1], ay = y - C.ext[2], by = y - C.ext[3];
+        const double ss[4] = {fma(ax, ax, ay * ay), fma(ax, ax, by * by), fma(bx, bx, ay * ay),
+                              fma(bx, bx, by * by)};
+        double R0 = 0.0, R1 = 0.0, R2 = 0.0, R3 = 0.0, R4 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double a = ss[i] + zc2, yi = rsqrt_d(a);
+            const double y2 = yi * yi, y3 = y2 * yi, y5 = y3 * y2, y7 = y5 * y2;
+            R0 += a * yi;
+            R1 += yi;
+            R2 += ss[i] * y3;
+            R3 += ss[i] * y5;
+            R4 += ss[i] * fma(4.0, zc2, -ss[i]) * y7;
+        }
+        R1 *= zc;
+        R2 *= 0.5;
+        R3 *= -0.5 * zc;
+        R4 *= 0.125;
+        const double U0 = fma(R0, R0, -C.gap), U1 = 2.0 * R0 * R1, U2 = fma(R1, R1, 2.0 * R0 * R2);
+        const double U3 = 2.0 * fma(R0, R3, R1 * R2), U4 = fma(2.0 * R0, R4, fma(2.0 * R1, R3, R2 * R2));
+        const double w = rsqrt_d(U0), hw = 0.5 * w;
+        const double S0 = U0 * w, S1 = U1 * hw, S2 = fma(-S1, S1, U2) * hw;
+        const double S3 = fma(-2.0 * S1, S2, U3) * hw, S4 = (U4 - 2.0 * S1 * S3 - S2 * S2) * hw;
+        const double cn0 = (fma(g.c_nhi, S0, -g.c_nlo * R0) - C.o_n) * inv_step;
+        const double I0d = fmin(fmax(floor(cn0), -1048576.0), 1048576.0);
+        const int I0 = (int)I0d;
+        const float f0 = (float)(cn0 - I0d);
+        const float n1 = (float)(fma(g.c_nhi, S1, -g.c_nlo * R1) * inv_step * sz);
+        const float n2 = (float)(fma(g.c_nhi, S2, -g.c_nlo * R2) * inv_step * sz2);
+        const float n3 = (float)(fma(g.c_nhi, S3, -g.c_nlo * R3) * inv_step * sz3);
+        const float n4 = (float)(fma(g.c_nhi, S4, -g.c_nlo * R4) * inv_step * sz4);
+        const float n_lo = (float)(lo - I0), n_hi = (float)(C.nn - 1 - lo - I0);
+        const float n_base_hi = (float)(C.nn - (KERNEL ? 3 : 2) - I0);
+        const double ph0 = 0.25 * fma(g.k_max, S0, g.k_min * R0);
+        const float p0 = (float)fma(-6.283185307179586, rint(ph0 * 0.15915494309189535), ph0);
+        const float p1 = (float)(0.25 * fma(g.k_max, S1, g.k_min * R1) * sz);
+        const float p2 = (float)(0.25 * fma(g.k_max, S2, g.k_min * R2) * sz2);
+        const float p3 = (float)(0.25 * fma(g.k_max, S3, g.k_min * R3) * sz3);
+        const float p4 = (float)(0.25 * fma(g.k_max, S4, g.k_min * R4) * sz4);
+        // ---- u, v coordinates: float32 series of 1 / (d_a + d_b)
+        const float axf = xf - C.ef[0], bxf = xf - C.ef[1], ayf = yf - C.ef[2], byf = yf - C.ef[3];
+        const float dx0 = axf < 0.f ? axf : (bxf > 0.f ? bxf : 0.f);  // x - clip(x, e0, e1)
+        const float dy0 = ayf < 0.f ? ayf : (byf > 0.f ? byf : 0.f);
+        float cu_k[5], cv_k[5];
+        {
+            const float qs[4] = {fmaf(axf, axf, dy0 * dy0), fmaf(bxf, bxf, dy0 * dy0),
+                                 fmaf(ayf, ayf, dx0 * dx0), fmaf(byf, byf, dx0 * dx0)};
+            float D[2][5];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int m = 0; m < 5; ++m) D[h][m] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float a = qs[i] + zc2f, yi = rsqrt_approx(a);
+                const float y2 = yi * yi, y3 = y2 * yi, y5 = y3 * y2, y7 = y5 * y2;
+                float *Dh = D[i >> 1];
+                Dh[0] += a * yi;
+                Dh[1] += zcf * yi;
+                Dh[2] += 0.5f * qs[i] * y3;
+                Dh[3] += -0.5f * qs[i] * zcf * y5;
+                Dh[4] += 0.125f * qs[i] * fmaf(4.f, zc2f, -qs[i]) * y7;
+            }
+            const float num[2] = {C.ku * (axf + bxf), C.kv * (ayf + byf)};
+            const float off[2] = {C.ou, C.ov};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float Cr[5];
+                const float inv = rcp_approx(D[h][0]);
+                Cr[0] = inv;
+#pragma unroll
+                for (int m = 1; m < 5; ++m) {
+                    float acc_m = 0.f;
+#pragma unroll
+                    for (int q = 1; q <= m; ++q) acc_m = fmaf(D[h][q], Cr[m - q], acc_m);
+                    Cr[m] = -acc_m * inv;
+                }
+                float *o = h ? cv_k : cu_k;
+                o[0] = fmaf(num[h], Cr[0], off[h]);
+                o[1] = num[h] * Cr[1] * szf;
+                o[2] = num[h] * Cr[2] * sz2f;
+                o[3] = num[h] * Cr[3] * sz3f;
+                o[4] = num[h] * Cr[4] * sz4f;
+            }
+        }
+        // ---- the block's voxels
+#pragma unroll
+        for (int j = 0; j < ZQ; ++j) {
+            const float t = (float)j - 0.5f * (float)(ZQ - 1);
+            const float cu = fmaf(t, fmaf(t, fmaf(t, fmaf(t, cu_k[4], cu_k[3]), cu_k[2]), cu_k[1]), cu_k[0]);
+            const float cv = fmaf(t, fmaf(t, fmaf(t, fmaf(t, cv_k[4], cv_k[3]), cv_k[2]), cv_k[1]), cv_k[0]);
+            const float cf = fmaf(t, fmaf(t, fmaf(t, fmaf(t, n4, n3), n2), n1), f0);
+            if (!(cu >= (float)lo && cu <= C.hu + 1.f && cv >= (float)lo && cv <= C.hv + 1.f &&
+                  cf >= n_lo && cf <= n_hi)) {
+                good &= ~(1u << j);
+                continue;
+            }
+            int iu, iv;
+            float fu, fv;
+            split_f(cu, C.hu, iu, fu);
+            split_f(cv, C.hv, iv, fv);
+            float bn = __fadd_rd(cf, 12582912.0f) - 12582912.0f;  // floor(cf)
+            bn = fminf(bn, n_base_hi);                              // top edge: base hi, fraction 1
+            const int iw = I0 + (int)bn;
+            const float fn = cf - bn;
+            const float2 smp = kp ? gather_child_pairs<KERNEL>(kp, C, iu, iv, iw, fu, fv, fn)
+                                  : gather_child<KERNEL>(kv, C, iu, iv, iw, fu, fv, fn);
+            const float ph = fmaf(t, fmaf(t, fmaf(t, fmaf(t, p4, p3), p2), p1), p0);
+            const float nr = fmaf(ph, 0.15915494f, 12582912.0f) - 12582912.0f;
+            const float red = fmaf(nr, 1.7484555e-7f, fmaf(nr, -6.28318548f, ph));
+            float sn, cs;
+            __sincosf(red, &sn, &cs);
+            cfma(acc[j], smp, make_float2(cs, sn));
+        }
+    }
+    const int64_t v0 = row * nz + k * ZQ;
+    unsigned fl;
+    if (k * ZQ + ZQ <= nz && v0 >= vb && v0 + ZQ <= ve) {  // the whole block is in range
+        fl = ZQ - __popc(good);
+#pragma unroll
+        for (int j = 0; j < ZQ; ++j)
+            out[v0 + j - vb] = ((good >> j) & 1u) ? acc[j] : make_float2(0.f, 0.f);
+    } else {
+        fl = 0;
+#pragma unroll
+        for (int j = 0; j < ZQ; ++j) {
+            const int64_t v = v0 + j;
+            if (!(k * ZQ + j < nz && v >= vb && v < ve)) continue;
+            const bool ok = (good >> j) & 1u;
+            fl += !ok;
+            out[v - vb] = ok ? acc[j] : make_float2(0.f, 0.f);
+        }
+    }
+    warp_add(flagged, fl);
+}
+
 // Per-child constants for a merge launch (stream-ordered scratch).
 static int prep_children(const hhsar_grid_desc *kids, int64_t n, const hhsar_geom &g, int kernel,
                          MergeChild **out, cudaStream_t s,
@@ -455,11 +711,13 @@ extern "C" int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, 
 extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, const int64_t *dims,
                                      int64_t vox_begin, int64_t vox_end,
                                      const hhsar_grid_desc *child_grids, int64_t n_children,
-                                     const void *child_values, const hhsar_geom *geom, int kernel,
+                                     const void *child_values, int64_t span_begin,
+                                     int64_t span_points, const hhsar_geom *geom, int kernel,
                                      void *out, int64_t *flagged, void *stream) {
     HHSAR_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0 && n_children > 0 && geom,
                   "merge_cartesian: bad arguments");
     HHSAR_REQUIRE(kernel == 0 || kernel == 1, "merge_cartesian: unknown interpolation kernel");
+    HHSAR_REQUIRE(span_begin >= 0 && span_points >= 0, "merge_cartesian: bad child span");
     const int64_t total = dims[0] * dims[1] * dims[2];
     if (vox_end < 0 || vox_end > total) vox_end = total;
     HHSAR_REQUIRE(vox_begin >= 0 && vox_begin <= vox_end, "merge_cartesian: bad voxel range");
@@ -481,6 +739,54 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
                                               vox_begin, vox_end, q0, q1 - q0, kids,
                                               (int)n_children, kv, *geom, o, flagged);
     };
+#ifndef HHSAR_LANDING_EXACT
+    // z series (merge_cartesian_series_kernel): ZQ z voxels per thread with
+    // the Taylor offset |z - z_c| <= (ZQ - 1) sz / 2 at most 6% of the
+    // nearest voxel's height above the aperture plane (every distance the
+    // series expands is >= z): fifth-order terms below ~1e-5 rad of phase
+    const double oz = origin[2], sz = step[2];
+#ifndef HHSAR_LANDING_ZQ
+#define HHSAR_LANDING_ZQ 8
+#endif
+    // (cubic: 64-point stencils, at most 4 voxels per thread for registers)
+    const int zq = (HHSAR_LANDING_ZQ >= 8 && kernel == 0 && oz > 0.0 && 3.5 * sz <= 0.06 * oz) ? 8
+                   : (oz > 0.0 && 1.5 * sz <= 0.06 * oz)                      ? 4
+                                                                             : 0;
+    if (zq) {
+        // pair-staged copy of the children's lattices (16 B per point): the
+        // gathers then move half as many L1 wavefronts
+        float4 *pairs = nullptr;
+        if (span_points > 0) {
+            if (cudaMallocAsync(&pairs, span_points * sizeof(float4), s) != cudaSuccess) {
+                cudaFreeAsync(kids, s);
+                return set_error(HHSAR_ECUDA, "merge_cartesian: pair scratch allocation failed");
+            }
+            pair_rows_kernel<<<(unsigned)((span_points + 255) / 256), 256, 0, s>>>(
+                kv, span_begin, span_points, pairs);
+        }
+        const float4 *kp = pairs ? pairs - span_begin : nullptr;  // indexed by pool offset
+        auto launch_s = [&](auto kern) {
+            const int64_t nzq = (dims[2] + zq - 1) / zq;
+            const int64_t q0 = (vox_begin / dims[2]) * nzq + (vox_begin % dims[2]) / zq;
+            const int64_t q1 = ((vox_end - 1) / dims[2]) * nzq + ((vox_end - 1) % dims[2]) / zq + 1;
+            const unsigned blocks = (unsigned)((q1 - q0 + MERGE_THREADS - 1) / MERGE_THREADS);
+            kern<<<blocks, MERGE_THREADS, 0, s>>>(origin[0], origin[1], origin[2], step[0], step[1],
+                                                  step[2], (int)dims[1], (int)dims[2], vox_begin,
+                                                  vox_end, q0, q1 - q0, kids, (int)n_children, kv,
+                                                  kp, *geom, o, flagged);
+        };
+        if (kernel == 0) {
+            if (zq == 8) launch_s(merge_cartesian_series_kernel<0, 8>);
+            else launch_s(merge_cartesian_series_kernel<0, 4>);
+        } else {
+            launch_s(merge_cartesian_series_kernel<1, 4>);
+        }
+        rc = check_launch("merge_cartesian_series_kernel");
+        if (pairs) cudaFreeAsync(pairs, s);
+        cudaFreeAsync(kids, s);
+        return rc;
+    }
+#endif
     // 4 z-voxels per thread when there are >= 4 children or the launch is
     // large (config 4, 268 M voxels x 2 children: 4.49 -> 4.19 ms); 2
     // otherwise (config 3, 33.5 M voxels: 0.61 ms vs 0.62).  Two children

@@ -173,6 +173,11 @@ _GEOMS = {}
 # device lattices
 # ---------------------------------------------------------------------------
 
+# the landing gathers from a (v[i], v[i+1]) pair-staged copy of the top
+# lattices (hhsar_merge_cartesian span arguments); False gathers directly
+LANDING_PAIRS = True
+
+
 class Lattices:
     """All grids of a schedule on the device: descriptors + global pools.
 
@@ -469,9 +474,13 @@ class Pipeline:
         vol = torch.empty(ve - vb, dtype=torch.complex64, device=self.dev)
         c0, c1 = self.sched.level_slices[-1]
         d = np.asarray(self.final_dims, dtype=np.int64)
+        span0 = int(self.lat.descs["offset"][c0])  # the children's pool span (pair staging)
+        span = int(self.lat.descs["offset"][c1 - 1]) + int(self.lat.npts[c1 - 1]) - span0
+        if not LANDING_PAIRS:
+            span = 0
         _native.call("hhsar_merge_cartesian", _native.ptr(np.ascontiguousarray(origin)),
                      _native.ptr(np.ascontiguousarray(step)), _native.ptr(d), vb, ve,
-                     self.lat.desc_ptr(c0), c1 - c0, _native.ptr(self.values),
+                     self.lat.desc_ptr(c0), c1 - c0, _native.ptr(self.values), span0, span,
                      _native.ptr(self.lat.geom), self.kid, _native.ptr(vol),
                      _native.c_void_p_offset(self.flags, self.n_stages), _native.stream_handle())
         return vol
