@@ -17,6 +17,10 @@ namespace hhsar {
 
 constexpr int MERGE_THREADS = 128;
 
+#ifndef HHSAR_LANDING_TILE
+#define HHSAR_LANDING_TILE 16  // landing: a warp's columns (x 32 / TILE z blocks); 0: linear order
+#endif
+
 __device__ __forceinline__ int find_by_offset(const hhsar_grid_desc *__restrict__ grids, int n,
                                               int64_t key) {
     int lo = 0, hi = n - 1;
@@ -437,13 +441,26 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
                               const MergeChild *__restrict__ kids, int nk,
                               const float2 *__restrict__ kv, const float4 *__restrict__ kp,
                               hhsar_geom g, float2 *__restrict__ out,
-                              int64_t *__restrict__ flagged) {
+                              int64_t *__restrict__ flagged, int tile) {
     const int64_t qi = (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
     if (qi >= nq) return;
     const int nzq = (nz + ZQ - 1) / ZQ;
-    const int64_t Q = q0 + qi;           // global block: column (ix, iy), z block k
-    const int64_t row = Q / nzq;
-    const int k = (int)(Q - row * nzq);
+    int64_t row;  // column (ix, iy)
+    int k;        // z block
+    if (tile) {
+        // a warp takes 4 adjacent columns x 8 adjacent z blocks: its lanes'
+        // taps share lattice rows and lines (the launcher checks alignment)
+        constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1, TK = 32 / TC;
+        const int64_t w = qi >> 5;
+        const int lane = (int)(qi & 31), kt_per = nzq / TK;
+        const int64_t rg = w / kt_per;
+        row = q0 / nzq + rg * TC + lane / TK;
+        k = (int)(w - rg * kt_per) * TK + lane % TK;
+    } else {
+        const int64_t Q = q0 + qi;
+        row = Q / nzq;
+        k = (int)(Q - row * nzq);
+    }
     const int iy = (int)(row % ny), ix = (int)(row / ny);
     const double x = __dadd_rn(ox, __dmul_rn(sx, (double)ix));
     const double y = __dadd_rn(oy, __dmul_rn(sy, (double)iy));
@@ -748,6 +765,7 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
 #ifndef HHSAR_LANDING_ZQ
 #define HHSAR_LANDING_ZQ 8
 #endif
+
     // (cubic: 64-point stencils, at most 4 voxels per thread for registers)
     const int zq = (HHSAR_LANDING_ZQ >= 8 && kernel == 0 && oz > 0.0 && 3.5 * sz <= 0.06 * oz) ? 8
                    : (oz > 0.0 && 1.5 * sz <= 0.06 * oz)                      ? 4
@@ -770,10 +788,13 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
             const int64_t q0 = (vox_begin / dims[2]) * nzq + (vox_begin % dims[2]) / zq;
             const int64_t q1 = ((vox_end - 1) / dims[2]) * nzq + ((vox_end - 1) % dims[2]) / zq + 1;
             const unsigned blocks = (unsigned)((q1 - q0 + MERGE_THREADS - 1) / MERGE_THREADS);
+            constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1;
+            const int tile = HHSAR_LANDING_TILE > 0 && nzq % (32 / TC) == 0 &&
+                             q0 % (TC * nzq) == 0 && (q1 - q0) % (TC * nzq) == 0;
             kern<<<blocks, MERGE_THREADS, 0, s>>>(origin[0], origin[1], origin[2], step[0], step[1],
                                                   step[2], (int)dims[1], (int)dims[2], vox_begin,
                                                   vox_end, q0, q1 - q0, kids, (int)n_children, kv,
-                                                  kp, *geom, o, flagged);
+                                                  kp, *geom, o, flagged, tile);
         };
         if (kernel == 0) {
             if (zq == 8) launch_s(merge_cartesian_series_kernel<0, 8>);
