@@ -74,7 +74,7 @@ __device__ __forceinline__ float lp_sqrt(float x) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(LP_THREADS)
+__global__ void __launch_bounds__(LP_THREADS, 6)  // 6 CTAs per SM (40 registers)
 leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
                    const int32_t *__restrict__ idx, const int32_t *__restrict__ cnt,
                    const double *__restrict__ positions, const float4 *__restrict__ el,
@@ -159,6 +159,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     for (int64_t c0 = 0; c0 < m; c0 += LP_CHUNK) {
         const int cn = (int)min((int64_t)LP_CHUNK, m - c0);
         __syncthreads();
+        int el_fast = 1;
         if (t < cn) {
             const float4 e = el[e0 + c0 + t];
             const float ex = e.x - cx, ey = e.y - cy, ez = e.z - cz;
@@ -176,8 +177,10 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
             s_el[t] = make_float4(e.x, e.y, e.z, __int_as_float(fast ? (int)off : -1));
             s_lo[t] = fast ? los : -1;
             s_row[t] = (e0 + c0 + t) * (int64_t)k.n_t;
+            el_fast = fast;
         }
-        __syncthreads();
+        // block-uniform: every element of the chunk takes the staged path
+        const bool all_fast = __syncthreads_and(el_fast);
 #pragma unroll 2
         for (int q = t; q < cn * TW; q += LP_THREADS) {
             const int j = q >> lw, lo = s_lo[j];
@@ -246,6 +249,15 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         // elements two at a time (loop overhead and the element load shared;
         // two independent unit chains in flight)
         int j = warp_live ? 0 : cn;  // warps without points only stage
+        if (all_fast) {  // the common case: no per-element path test
+            for (; j + 3 < cn; j += 4) {
+                const float4 ea = s_el[j], eb = s_el[j + 1], ec = s_el[j + 2], ed = s_el[j + 3];
+                fast_unit(ea);
+                fast_unit(eb);
+                fast_unit(ec);
+                fast_unit(ed);
+            }
+        }
         for (; j + 1 < cn; j += 2) {
             const float4 ea = s_el[j], eb = s_el[j + 1];
             if (__float_as_int(ea.w) != -1 && __float_as_int(eb.w) != -1) {
