@@ -269,7 +269,10 @@ int hhsar_downconvert(const hhsar_grid_desc *grids, int64_t n_grids, int64_t n_p
  * children's lattices occupy pool points [span_begin, span_begin +
  * span_points) of child_values; with span_points > 0 the landing stages a
  * 16-byte (v[i], v[i+1]) pair copy of that span for its gathers
- * (span_points = 0: gathers from child_values directly). */
+ * (span_points = 0: gathers from child_values directly).  The z-series
+ * evaluation is used where its truncation is negligible; kernel |
+ * HHSAR_LANDING_PER_VOXEL forces the per-voxel float64 form. */
+#define HHSAR_LANDING_PER_VOXEL 16
 int hhsar_merge_cartesian(const double *origin, const double *step, const int64_t *dims,
                           int64_t vox_begin, int64_t vox_end,
                           const hhsar_grid_desc *child_grids, int64_t n_children,

@@ -733,6 +733,8 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
                                      void *out, int64_t *flagged, void *stream) {
     HHSAR_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0 && n_children > 0 && geom,
                   "merge_cartesian: bad arguments");
+    const bool per_voxel = (kernel & HHSAR_LANDING_PER_VOXEL) != 0;
+    kernel &= ~HHSAR_LANDING_PER_VOXEL;
     HHSAR_REQUIRE(kernel == 0 || kernel == 1, "merge_cartesian: unknown interpolation kernel");
     HHSAR_REQUIRE(span_begin >= 0 && span_points >= 0, "merge_cartesian: bad child span");
     const int64_t total = dims[0] * dims[1] * dims[2];
@@ -767,9 +769,10 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
 #endif
 
     // (cubic: 64-point stencils, at most 4 voxels per thread for registers)
-    const int zq = (HHSAR_LANDING_ZQ >= 8 && kernel == 0 && oz > 0.0 && 3.5 * sz <= 0.06 * oz) ? 8
-                   : (oz > 0.0 && 1.5 * sz <= 0.06 * oz)                      ? 4
-                                                                             : 0;
+    const int zq = per_voxel ? 0
+                   : (HHSAR_LANDING_ZQ >= 8 && kernel == 0 && oz > 0.0 && 3.5 * sz <= 0.06 * oz) ? 8
+                   : (oz > 0.0 && 1.5 * sz <= 0.06 * oz) ? 4
+                                                        : 0;
     if (zq) {
         // pair-staged copy of the children's lattices (16 B per point): the
         // gathers then move half as many L1 wavefronts

@@ -176,6 +176,10 @@ _GEOMS = {}
 # the landing gathers from a (v[i], v[i+1]) pair-staged copy of the top
 # lattices (hhsar_merge_cartesian span arguments); False gathers directly
 LANDING_PAIRS = True
+# the landing evaluates z runs by series where accurate (hhsar_merge_cartesian
+# picks); False forces the per-voxel float64 form (HHSAR_LANDING_PER_VOXEL)
+LANDING_SERIES = True
+LANDING_PER_VOXEL = 16
 
 
 class Lattices:
@@ -481,7 +485,8 @@ class Pipeline:
         _native.call("hhsar_merge_cartesian", _native.ptr(np.ascontiguousarray(origin)),
                      _native.ptr(np.ascontiguousarray(step)), _native.ptr(d), vb, ve,
                      self.lat.desc_ptr(c0), c1 - c0, _native.ptr(self.values), span0, span,
-                     _native.ptr(self.lat.geom), self.kid, _native.ptr(vol),
+                     _native.ptr(self.lat.geom),
+                     self.kid | (0 if LANDING_SERIES else LANDING_PER_VOXEL), _native.ptr(vol),
                      _native.c_void_p_offset(self.flags, self.n_stages), _native.stream_handle())
         return vol
 

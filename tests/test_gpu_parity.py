@@ -506,3 +506,39 @@ def test_sdc_phase_operator_vs_reference(hh, small):
     got = vals.cpu().numpy().astype(np.complex128)
     want = np.exp(-1j * z["map_phase"])
     assert np.max(np.abs(got - want)) < 2e-6
+
+
+@pytest.mark.parametrize("config,kernel", [(2, "linear"), (3, "linear"), (2, "cubic")])
+def test_landing_series_equals_per_voxel(config, kernel):
+    """The z-series landing (merge_cartesian_series_kernel: quartic Taylor
+    polynomials per 8-voxel z run, pair-staged lattice gathers) against the
+    per-voxel float64 landing (HHSAR_LANDING_PER_VOXEL) on the same device
+    lattices: same image to float32 rounding, same flags; pair staging on
+    or off gives the same bits for the linear kernel."""
+    import torch
+    from paper_2506_23568_b200 import bpa, ffbp, workloads
+    w = workloads.config(config)
+    gen = torch.Generator(device="cuda").manual_seed(w.seed)
+    cube = torch.randn((w.n_elements, w.freqs.count), dtype=torch.complex64, device="cuda",
+                       generator=gen)
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    params = ffbp.FfbpParams(levels=w.levels, kernel=kernel)
+    args = (cube, el, bpa.el_f32x4(el), w.freqs, w.region, w.dims, params, w.levels,
+            w.merge_factor, w.upsample)
+    out = {}
+    try:
+        for series, pairs in ((True, True), (True, False), (False, True)):
+            ffbp.LANDING_SERIES, ffbp.LANDING_PAIRS = series, pairs
+            run = ffbp.hhffbpa_from_cube(*args)
+            out[series, pairs] = (run.volume.cpu().numpy(), int(run.flags.cpu()[-1]))
+    finally:
+        ffbp.LANDING_SERIES, ffbp.LANDING_PAIRS = True, True
+    ref, ref_flags = out[False, True]
+    got, flags = out[True, True]
+    assert flags == ref_flags
+    assert rel_l2(got, ref) < 5e-5
+    assert np.argmax(np.abs(got)) == np.argmax(np.abs(ref))
+    if kernel == "linear":
+        assert np.array_equal(out[True, False][0], got)
+    else:
+        assert rel_l2(out[True, False][0], got) < 1e-6
