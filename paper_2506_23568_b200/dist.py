@@ -376,7 +376,8 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     """
     import torch
     from .bpa import el_f32x4
-    from .ffbp import Pipeline, finish_lattices, plan_lattices, src_pad_of
+    from .ffbp import (NEWTON_FIRST_MAX_COLUMNS, Pipeline, finish_lattices, geometry_stream,
+                       plan_lattices, src_pad_of)
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     world, rank = comm.world, comm.rank
     sched, kx, owned, _ = plan_shard(el_dev.shape[0], levels, merge_factor, world, rank)
@@ -387,15 +388,26 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         mask[a:b] = True
     n_t, dt, _, _ = profile_axis(kgrid, upsample)
     window_hi = (n_t - 1) * dt
-    pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
-                            src_pad_of(params), window_hi, gate_dt=dt if gate else None,
-                            gate_bins=n_t)
+    # as ffbp.hhffbpa_from_cube: plan and Newton on the high-priority
+    # geometry stream, the (gated) range compression on the caller's stream
+    # beside Newton
+    main = torch.cuda.current_stream()
+    geo = geometry_stream(el_dev.device)
+    geo.wait_stream(main)
+    with torch.cuda.stream(geo):
+        pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
+                                src_pad_of(params), window_hi, gate_dt=dt if gate else None,
+                                gate_bins=n_t)
     if callable(upload):
         upload = upload()
         cube_dev_rows = upload.tensor
-    lat = finish_lattices(pending, newton_grids=mask)
+    lat = None
     if gate:
-        b0, w = lat.gate
+        pending["done"].synchronize()
+        n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
+        if n_cols <= NEWTON_FIRST_MAX_COLUMNS or upload is not None:
+            with torch.cuda.stream(geo):
+                lat = finish_lattices(pending, newton_grids=mask)
         env, t0, dt, k_ref = range_compress_window(
             cube_dev_rows, kgrid, upsample, b0, w, chunks=upload.chunks if upload else None,
             row0=e_row0)
@@ -404,6 +416,12 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
             upload.wait()
         env, dt, k_ref = range_compress_device(cube_dev_rows, kgrid, upsample)
         t0 = 0.0
+    if lat is None:
+        with torch.cuda.stream(geo):
+            lat = finish_lattices(pending, newton_grids=mask)
+    main.wait_stream(geo)
+    for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
+        t.record_stream(main)
     pipe = Pipeline(env, el_dev, el_f32x4(el_dev), t0, dt, k_ref, kgrid, region, final_dims,
                     params, levels, merge_factor, window_hi, newton_grids=mask,
                     env_row0=e_row0, sched=sched, lat=lat)
