@@ -221,6 +221,11 @@ __device__ __forceinline__ f2x add2(f2x a, f2x b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
     return d;
 }
+__device__ __forceinline__ f2x add2_rm(f2x a, f2x b) {  // round toward -inf
+    f2x d;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));
+    return d;
+}
 __device__ __forceinline__ f2x sub2(f2x a, f2x b) {
     f2x d;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.r) : "l"(a.r), "l"(b.r));

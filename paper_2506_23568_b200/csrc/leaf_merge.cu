@@ -170,8 +170,9 @@ __device__ __forceinline__ float2 gather_child(const float2 *__restrict__ vals, 
 }
 
 // The same gather from the pair-staged copy of the child lattices: entry i
-// holds (v[i], v[i + 1]) in 16 B, so each lattice row of the stencil is one
-// 128-bit load (linear: 4 per sample instead of 8; cubic: 32 instead of 64).
+// holds (v[i], v[i + 1] - v[i]) in 16 B, so each lattice row of the stencil
+// is one 128-bit load (linear: 4 per sample instead of 8; cubic: 32 instead
+// of 64).
 template <int KERNEL>
 __device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ pairs,
                                                      const MergeChild &C, int iu, int iv, int iw,
@@ -187,9 +188,8 @@ __device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ 
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int bb = 0; bb < 2; ++bb) {
-                const float4 v = __ldg(base + idx[a][bb]);
-                const f2x x0 = pk2(v.x, v.y);
-                r[a][bb] = fma2(bc2(fn), sub2(pk2(v.z, v.w), x0), x0);
+                const float4 v = __ldg(base + idx[a][bb]);  // (v[i], v[i+1] - v[i])
+                r[a][bb] = fma2(bc2(fn), pk2(v.z, v.w), pk2(v.x, v.y));
             }
         const f2x s0 = fma2(bc2(fv), sub2(r[0][1], r[0][0]), r[0][0]);
         const f2x s1 = fma2(bc2(fv), sub2(r[1][1], r[1][0]), r[1][0]);
@@ -208,7 +208,11 @@ __device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ 
             for (int bb = 0; bb < 4; ++bb) {
                 const float4 *row = b + a * su + bb * C.nn;
                 const float w = wu[a] * wv[bb];
-                const float4 p0 = __ldg(row), p1 = __ldg(row + 2);
+                float4 p0 = __ldg(row), p1 = __ldg(row + 2);  // (v[i], v[i+1] - v[i]) pairs
+                p0.z += p0.x;
+                p0.w += p0.y;
+                p1.z += p1.x;
+                p1.w += p1.y;
                 acc.x = fmaf(p0.x, w * wn[0], fmaf(p0.z, w * wn[1], fmaf(p1.x, w * wn[2], fmaf(p1.z, w * wn[3], acc.x))));
                 acc.y = fmaf(p0.y, w * wn[0], fmaf(p0.w, w * wn[1], fmaf(p1.y, w * wn[2], fmaf(p1.w, w * wn[3], acc.y))));
             }
@@ -216,13 +220,14 @@ __device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ 
     }
 }
 
-// pairs[i - begin] = (v[i], v[i + 1]) for the child lattices' pool span
+// pairs[i - begin] = (v[i], v[i + 1] - v[i]) for the child lattices' pool
+// span: the n-lerp of a stencil row is then one packed FMA
 __global__ void pair_rows_kernel(const float2 *__restrict__ vals, int64_t begin, int64_t n,
                                  float4 *__restrict__ pairs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float2 a = vals[begin + i], b = vals[begin + (i + 1 < n ? i + 1 : i)];
-    pairs[i] = make_float4(a.x, a.y, b.x, b.y);
+    pairs[i] = make_float4(a.x, a.y, b.x - a.x, b.y - a.y);
 }
 
 // Lattice interpolation with the reference's hull rules (_kernels.py:117-189)
@@ -564,29 +569,47 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
                 o[4] = num[h] * Cr[4] * sz4f;
             }
         }
-        // ---- the block's voxels
+        // ---- the block's voxels: (u, v) and (n, phase) as packed pairs
+        f2x uv_k[5], np_k[5];
+        uv_k[0] = pk2(cu_k[0], cv_k[0]);
+        np_k[0] = pk2(f0, p0);
+        uv_k[1] = pk2(cu_k[1], cv_k[1]);
+        np_k[1] = pk2(n1, p1);
+        uv_k[2] = pk2(cu_k[2], cv_k[2]);
+        np_k[2] = pk2(n2, p2);
+        uv_k[3] = pk2(cu_k[3], cv_k[3]);
+        np_k[3] = pk2(n3, p3);
+        uv_k[4] = pk2(cu_k[4], cv_k[4]);
+        np_k[4] = pk2(n4, p4);
+        const f2x magic2 = bc2(12582912.0f);
 #pragma unroll
         for (int j = 0; j < ZQ; ++j) {
-            const float t = (float)j - 0.5f * (float)(ZQ - 1);
-            const float cu = fmaf(t, fmaf(t, fmaf(t, fmaf(t, cu_k[4], cu_k[3]), cu_k[2]), cu_k[1]), cu_k[0]);
-            const float cv = fmaf(t, fmaf(t, fmaf(t, fmaf(t, cv_k[4], cv_k[3]), cv_k[2]), cv_k[1]), cv_k[0]);
-            const float cf = fmaf(t, fmaf(t, fmaf(t, fmaf(t, n4, n3), n2), n1), f0);
+            const f2x tt = bc2((float)j - 0.5f * (float)(ZQ - 1));
+            const f2x uv = fma2(tt, fma2(tt, fma2(tt, fma2(tt, uv_k[4], uv_k[3]), uv_k[2]), uv_k[1]),
+                                uv_k[0]);
+            const f2x np = fma2(tt, fma2(tt, fma2(tt, fma2(tt, np_k[4], np_k[3]), np_k[2]), np_k[1]),
+                                np_k[0]);
+            const float cu = lo2(uv), cv = hi2(uv), cf = lo2(np), ph = hi2(np);
             if (!(cu >= (float)lo && cu <= C.hu + 1.f && cv >= (float)lo && cv <= C.hv + 1.f &&
                   cf >= n_lo && cf <= n_hi)) {
                 good &= ~(1u << j);
                 continue;
             }
-            int iu, iv;
-            float fu, fv;
-            split_f(cu, C.hu, iu, fu);
-            split_f(cv, C.hv, iv, fv);
+            // floors of (u, v) by one round-down packed add (as split_f), the
+            // bases clamped to (hu, hv) (top edge: fraction 1)
+            const f2x fl2 = sub2(add2_rm(uv, magic2), magic2);
+            const f2x b2 = pk2(fminf(lo2(fl2), C.hu), fminf(hi2(fl2), C.hv));
+            const f2x bm = add2(b2, magic2);
+            const int iu = __float_as_int(lo2(bm)) - __float_as_int(12582912.0f);
+            const int iv = __float_as_int(hi2(bm)) - __float_as_int(12582912.0f);
+            const f2x fuv = sub2(uv, b2);
+            const float fu = lo2(fuv), fv = hi2(fuv);
             float bn = __fadd_rd(cf, 12582912.0f) - 12582912.0f;  // floor(cf)
             bn = fminf(bn, n_base_hi);                              // top edge: base hi, fraction 1
             const int iw = I0 + (int)bn;
             const float fn = cf - bn;
             const float2 smp = kp ? gather_child_pairs<KERNEL>(kp, C, iu, iv, iw, fu, fv, fn)
                                   : gather_child<KERNEL>(kv, C, iu, iv, iw, fu, fv, fn);
-            const float ph = fmaf(t, fmaf(t, fmaf(t, fmaf(t, p4, p3), p2), p1), p0);
             const float nr = fmaf(ph, 0.15915494f, 12582912.0f) - 12582912.0f;
             const float red = fmaf(nr, 1.7484555e-7f, fmaf(nr, -6.28318548f, ph));
             float sn, cs;
