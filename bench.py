@@ -344,6 +344,8 @@ def run_ours(args):
     graph = (ffbp.StepGraph(cube, el, el4, w.freqs, w.region, w.dims, params, w.levels,
                             w.merge_factor, w.upsample) if world == 1 else None)
 
+    shard_plan = {}
+
     def step(record=False):
         if world == 1:
             if not record:
@@ -353,9 +355,13 @@ def run_ours(args):
                                          w.levels, w.merge_factor, w.upsample, marks=m)
             marks.update(m)
             return run
-        return hdist.hhffbpa_sharded_device(comm, cube, e0, el, w.freqs, w.region, w.dims,
-                                            params, w.levels, w.merge_factor, w.upsample,
-                                            output="shard")
+        # N ranks: each rank's plan (its restricted Newton work list) is
+        # cached from the first (warm-up) step, so no step waits on the host
+        r = hdist.hhffbpa_sharded_device(comm, cube, e0, el, w.freqs, w.region, w.dims,
+                                         params, w.levels, w.merge_factor, w.upsample,
+                                         output="shard", plan_cache=shard_plan.get("plan"))
+        shard_plan.setdefault("plan", r.plan)
+        return r
 
     gpu = dev.index if world > 1 else int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0)
     with ClockSampler(gpu) as clocks:

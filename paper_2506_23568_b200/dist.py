@@ -351,7 +351,8 @@ class ShardedVolume(SimpleNamespace):
 
 def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, region, final_dims,
                            params, levels: int, merge_factor: int, upsample: int,
-                           gate: bool = True, output: str = "all", upload=None):
+                           gate: bool = True, output: str = "all", upload=None,
+                           plan_cache=None):
     """One rank's share of HHFFBPA:
 
     1. subaperture-group partition: the rank owns a contiguous run of
@@ -370,14 +371,17 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
 
     ``upload`` (rangecomp.CubeUpload of this rank's rows, or a zero-argument
     factory of one started right after the plan is queued; ``cube_dev_rows``
-    may then be None): compress chunk by chunk as rows land.  Returns a namespace: volume (flat complex64: the
-    whole volume where it was gathered, else this rank's slab), vox_range,
-    stats[G,6], flags, oow (identical on all ranks), sched, descs.
+    may then be None): compress chunk by chunk as rows land.  ``plan_cache``
+    (the ``plan`` of an earlier call of this rank with the same geometry):
+    no host wait on the plan (ffbp.PlanCache).  Returns a namespace: volume
+    (flat complex64: the whole volume where it was gathered, else this
+    rank's slab), vox_range, stats[G,6], flags, oow (identical on all
+    ranks), sched, descs, plan (this rank's PlanCache).
     """
     import torch
     from .bpa import el_f32x4
-    from .ffbp import (NEWTON_FIRST_MAX_COLUMNS, Pipeline, finish_lattices, geometry_stream,
-                       plan_lattices, src_pad_of)
+    from .ffbp import (NEWTON_FIRST_MAX_COLUMNS, Pipeline, PlanCache, finish_lattices,
+                       geometry_stream, plan_lattices, src_pad_of)
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     world, rank = comm.world, comm.rank
     sched, kx, owned, _ = plan_shard(el_dev.shape[0], levels, merge_factor, world, rank)
@@ -397,13 +401,14 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     with torch.cuda.stream(geo):
         pending = plan_lattices(el_dev, sched, region, kgrid, params.gamma, params.margin,
                                 src_pad_of(params), window_hi, gate_dt=dt if gate else None,
-                                gate_bins=n_t)
+                                gate_bins=n_t, cached=plan_cache)
     if callable(upload):
         upload = upload()
         cube_dev_rows = upload.tensor
     lat = None
     if gate:
-        pending["done"].synchronize()
+        if plan_cache is None:
+            pending["done"].synchronize()
         n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
         if n_cols <= NEWTON_FIRST_MAX_COLUMNS or upload is not None:
             with torch.cuda.stream(geo):
@@ -477,8 +482,9 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         flags[pipe.n_stages:] = fl
         oow = pipe.oow
     whole = output == "all" or world == 1 or (output == "root" and rank == 0)
+    plan = plan_cache if plan_cache is not None else PlanCache.of_lattices(pipe.lat)
     return SimpleNamespace(volume=vol, vox_range=(0, n_vox) if whole else (vb, ve), stats=stats,
-                           flags=flags, oow=oow, sched=sched, descs=pipe.lat.descs)
+                           flags=flags, oow=oow, sched=sched, descs=pipe.lat.descs, plan=plan)
 
 
 

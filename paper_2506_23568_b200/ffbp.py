@@ -349,8 +349,8 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     # (edited in place, uploaded from, kept alive with the lattices); a
     # cached plan brings its own copy
     if cached is not None:
-        if newton_grids is not None:
-            raise ValueError("a cached plan covers the whole schedule (no newton_grids)")
+        if (newton_grids is not None) != (cached.masked_dev is not None):
+            raise ValueError("a cached plan and newton_grids must come together")
         host = cached.descs
     else:
         host = p["host_d"].numpy().view(_native.GRID_DTYPE)
@@ -359,7 +359,12 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
         raise NumericDomainError("compressed coordinates undefined this close to the array plane")
     # offsets, column offsets and both totals came from the plan (device scan)
     total, n_cols, g_b0, g_w = (int(v) for v in status[8:40].view(np.int64))
-    if newton_grids is not None:
+    n_cols_masked = None
+    if newton_grids is not None and cached is not None:
+        # the cached restricted work list over the recomputed plan (D2D)
+        descs_dev.copy_(cached.masked_dev, non_blocking=True)
+        n_cols = n_cols_masked = cached.n_cols
+    elif newton_grids is not None:
         # Newton work list restricted to the selected grids: re-derive the
         # column offsets and send the descriptors back up
         span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
@@ -368,6 +373,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
         n_cols = int(starts[-1])
         host["col_offset"][0] = 0
         host["col_offset"][1:] = starts[:-1]
+        n_cols_masked = n_cols
         back, up = p["back"], p["keep"][1]
         nb = host.nbytes
         up[:nb].copy_(back[:nb], non_blocking=True)
@@ -388,6 +394,7 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     lat.keep = (p["back"], p["keep"][1])  # pinned staging must outlive the async copy
     lat.gate = (g_b0, g_w) if g_w > 0 else None
     lat.status = status
+    lat.n_cols_masked = n_cols_masked
     return lat
 
 
@@ -661,11 +668,25 @@ class PlanCache:
     its own (recomputed) plan."""
     descs: np.ndarray   # GRID_DTYPE [G] (pool / work-list offsets filled in)
     status: np.ndarray  # uint8 [40]: status word, totals, gate
+    # a plan whose Newton work list was restricted to some grids
+    # (newton_grids, the multi-GPU ranks): the restricted descriptor table on
+    # the device (copied over each recomputed plan) and its column count
+    masked_dev: object = None
+    n_cols: int = -1
 
     @staticmethod
     def of(run: DeviceRun) -> "PlanCache":
-        lat = run.lattices
-        return PlanCache(descs=lat.descs.copy(), status=np.asarray(lat.status).copy())
+        return PlanCache.of_lattices(run.lattices)
+
+    @staticmethod
+    def of_lattices(lat) -> "PlanCache":
+        import torch
+        descs = lat.descs.copy()
+        masked = None
+        if getattr(lat, "n_cols_masked", None) is not None:
+            masked = torch.as_tensor(descs.view(np.uint8)).to(lat.descs_dev.device)
+        return PlanCache(descs=descs, status=np.asarray(lat.status).copy(), masked_dev=masked,
+                         n_cols=-1 if masked is None else int(lat.n_cols_masked))
 
 
 class StepGraph:

@@ -139,3 +139,39 @@ def test_sharded_hhffbpa_own_rows_only(case):
     for vol in _run_world(4, rank):
         assert np.linalg.norm(vol.values - single.values) <= 1e-6 * np.linalg.norm(single.values)
         assert vol.provenance == single.provenance
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_sharded_device_step_with_cached_plan(case, world):
+    """The bench's N > 1 step: hhffbpa_sharded_device a second time with the
+    first call's plan (ffbp.PlanCache of the rank's restricted Newton work
+    list, no host wait on the plan) gives the same slab, stats and flags."""
+    import torch
+    import paper_2506_23568_b200 as hh
+    from paper_2506_23568_b200 import bpa, dist
+    w, cube = case
+    dims = (48, 48, 20)
+    params = hh.FfbpParams(levels=7)
+    values = np.asarray(cube.values)
+
+    def rank(comm):
+        dev = torch.device("cuda", 0)
+        el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+        e0, e1 = dist.plan_shard(el.shape[0], 7, 4, comm.world, comm.rank)[3]
+        rows = torch.as_tensor(values[e0:e1], device=dev)
+        runs = []
+        plan = None
+        for _ in range(3):
+            r = dist.hhffbpa_sharded_device(comm, rows, e0, el, w.freqs, w.region, dims, params,
+                                            7, 4, 4, output="shard", plan_cache=plan)
+            plan = r.plan
+            runs.append((r.volume.cpu().numpy(), r.stats.cpu().numpy(), r.flags.cpu().numpy(),
+                         r.vox_range))
+        return runs
+
+    for runs in _run_world(world, rank):
+        first = runs[0]
+        for again in runs[1:]:
+            assert again[3] == first[3]
+            assert np.array_equal(again[0], first[0])
+            assert np.array_equal(again[1], first[1]) and np.array_equal(again[2], first[2])
