@@ -18,7 +18,12 @@
 
 namespace hhsar {
 
-constexpr int LP_THREADS = 256;
+constexpr int LP_THREADS = 256;  // compact_leaf_kernel
+#ifndef HHSAR_LEAF_THREADS
+#define HHSAR_LEAF_THREADS 256
+#endif
+constexpr int LPT = HHSAR_LEAF_THREADS;  // leaf_points_kernel CTA (P points per thread)
+constexpr int LPT_MINB = 1536 / LPT;     // CTAs per SM at 40 registers
 constexpr float LP_MAGIC = 12582912.0f;
 constexpr unsigned LP_MAGIC_BITS = 0x4B400000u;
 
@@ -74,7 +79,7 @@ __device__ __forceinline__ float lp_sqrt(float x) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(LP_THREADS, 6)  // 6 CTAs per SM (40 registers)
+__global__ void __launch_bounds__(LPT, LPT_MINB)  // 1,536 threads per SM (40 registers)
 leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
                    const int32_t *__restrict__ idx, const int32_t *__restrict__ cnt,
                    const double *__restrict__ positions, const float4 *__restrict__ el,
@@ -87,11 +92,11 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __shared__ float4 s_el[WIN / 32];
     __shared__ int s_lo[WIN / 32];
     __shared__ int64_t s_row[WIN / 32];
-    __shared__ float s_box[2][LP_THREADS / 32];
+    __shared__ float s_box[2][LPT / 32];
     const int gi = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
     const hhsar_grid_desc &D = grids[gi];
     const int n = cnt[gi];
-    const int p0 = chunk * LP_THREADS * P;
+    const int p0 = chunk * LPT * P;
     if (p0 >= n) return;  // block-uniform
     const int t = threadIdx.x;
     // my points: P consecutive list entries per thread, so a partial last
@@ -128,14 +133,14 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __syncthreads();
     dmin = s_box[0][0];
     dmax = s_box[1][0];
-    for (int w = 1; w < LP_THREADS / 32; ++w) {
+    for (int w = 1; w < LPT / 32; ++w) {
         dmin = fminf(dmin, s_box[0][w]);
         dmax = fmaxf(dmax, s_box[1][w]);
     }
     // window width for this chunk (block-uniform): the widest window any of
     // the leaf's elements needs (same bounds as the staging below)
     int need = 0;
-    for (int64_t j = t; j < D.stop - D.start; j += LP_THREADS) {
+    for (int64_t j = t; j < D.stop - D.start; j += LPT) {
         const float4 e = el[D.start + j];
         const float ex = e.x - cx, ey = e.y - cy, ez = e.z - cz;
         const float re = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
@@ -148,7 +153,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
     __syncthreads();  // s_box reads above are done
     if ((t & 31) == 0) s_box[0][t >> 5] = __int_as_float(need);
     __syncthreads();
-    for (int w = 0; w < LP_THREADS / 32; ++w) need = max(need, __float_as_int(s_box[0][w]));
+    for (int w = 0; w < LPT / 32; ++w) need = max(need, __float_as_int(s_box[0][w]));
     const int lw = need <= 32 ? 5 : need <= 64 ? 6 : need <= 128 ? 7 : 8;  // log2 TW
     const int TW = 1 << lw, LP_CHUNK = WIN >> lw;
     f2x pa[P], pb[P];
@@ -182,7 +187,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         // block-uniform: every element of the chunk takes the staged path
         const bool all_fast = __syncthreads_and(el_fast);
 #pragma unroll 2
-        for (int q = t; q < cn * TW; q += LP_THREADS) {
+        for (int q = t; q < cn * TW; q += LPT) {
             const int j = q >> lw, lo = s_lo[j];
             if (lo < 0) continue;
             const int bin = lo + (q & (TW - 1));
@@ -316,9 +321,9 @@ int launch_leaf_points(const hhsar_grid_desc *grids, int64_t n_grids, int64_t ma
     // masked lattice points carry 0 (ffbp.py:174-175); valid ones are written below
     cudaMemsetAsync(values + pool_begin, 0, (pool_end - pool_begin) * sizeof(float2), s);
     compact_leaf_kernel<<<(unsigned)n_grids, LP_THREADS, 0, s>>>(grids, valid, idx, cnt);
-    const int chunks = (int)((max_points + LP_THREADS * P - 1) / (LP_THREADS * P));
+    const int chunks = (int)((max_points + LPT * P - 1) / (LPT * P));
     const unsigned blocks = (unsigned)(n_grids * chunks);
-    leaf_points_kernel<P><<<blocks, LP_THREADS, 0, s>>>(
+    leaf_points_kernel<P><<<blocks, LPT, 0, s>>>(
         grids, chunks, idx, cnt, positions, el, env, rot, k, g, downconvert, values, oow_total);
     cudaFreeAsync(idx, s);
     cudaFreeAsync(cnt, s);
