@@ -569,8 +569,8 @@ def _h2d_probe(host):
 
 def rc_roofline(w, run, rc_ms, step_ms):
     """Dominant kernel of the config-4 step: the range-gated compression
-    (range_compress_4096_kernel for 4,096-bin rows and a window of <= 512
-    bins, else range_compress_kernel).  Algorithmic bytes per launch = the cube read
+    (range_compress_split_kernel for 4,096- / 2,048-bin rows and a window of
+    <= 512 bins, else range_compress_kernel).  Algorithmic bytes per launch = the cube read
     once (N_el x n_f x 8 B) + the gated envelopes written once (N_el x w x 8
     B); also reported against the FFT's FP32 work."""
     from paper_2506_23568_b200 import ffbp, rangecomp
@@ -579,8 +579,9 @@ def rc_roofline(w, run, rc_ms, step_ms):
     by = w.n_elements * (w.freqs.count + gw) * 8.0
     kms = statistics.median(rc_ms) if rc_ms else None
     peak, src = _hbm_peak()
-    kname = ("range_compress_4096_kernel" if n_t == 4096 and w.freqs.count in (512, 1024)
-             and gw <= 512 else "range_compress_kernel")
+    split = ((n_t == 4096 and w.freqs.count in (512, 1024)) or
+             (n_t == 2048 and w.freqs.count in (256, 512))) and gw <= 512
+    kname = "range_compress_split_kernel" if split else "range_compress_kernel"
     out = {"kernel": kname, "bound": "hbm", "unit": "GB/s", "peak": peak,
            "algorithmic_bytes": int(by), "gate": [b0, gw, n_t]}
     if kms:

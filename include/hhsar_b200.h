@@ -175,9 +175,10 @@ int hhsar_range_compress(const void *cube, int64_t n_el, int64_t n_f, int64_t n_
 /* The same, keeping only delay bins [b0, b0 + w) of every row (a range
  * gate): out[n_el][w], out[e][i] = envelope[e][b0 + i].  Bins outside the
  * gate are neither stored nor, in the last radix-16 pass, computed; for
- * n_t = 4096 with n_f = 1024 or 512 and w <= 512 a 64 x 64 split with one
- * shared-memory exchange evaluates only the window's bins (a 4-point DFT
- * per 16-entry column slice, a 16-term Horner chain per bin).  An
+ * n_t = 4096 (n_f = 1024 or 512) and n_t = 2048 (n_f = 512 or 256) with
+ * w <= 512 a 64-column split with one shared-memory exchange evaluates only
+ * the window's bins (a 4- or 2-point DFT per 16-entry column slice, a
+ * 16-term Horner chain per bin).  An
  * envelope gated this way is a profile with t0' = t0 + b0 dt and w bins. */
 int hhsar_range_compress_window(const void *cube, int64_t n_el, int64_t n_f, int64_t n_t,
                                 double a, double dt, int64_t b0, int64_t w, void *out,

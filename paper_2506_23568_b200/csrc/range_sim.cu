@@ -336,18 +336,19 @@ int launch_rc(const float2 *cube, int64_t n_el, int n_f, const float2 *tw, const
 }
 
 // ---------------------------------------------------------------------------
-// Gated range compression of 4096-bin rows (BASELINE config 4: n_f = 1024
-// or 512 live samples, a window of a few hundred bins): one smem exchange
-// instead of the Stockham kernel's two.  With n = 64 n1 + n2 and
-// k = k1 + 64 k2,
+// Gated range compression of 4096- and 2048-bin rows (BASELINE configs 4
+// and 3: n_f = 1024 / 512 live samples, a window of a few hundred bins): one
+// smem exchange instead of the Stockham kernel's two.  With n = 64 n1 + n2
+// and k = k1 + KC k2 (KC = N / 64),
 //     X[k] = sum_{n2 < 64} W^{n2 k} A_{n2}[k1],
-//     A_{n2}[k1] = sum_{n1 < NL} x[64 n1 + n2] W64^{n1 k1}
-// (W = e^{+2 pi i / 4096}).  Stage A: thread n2 forms its column's 64
-// outputs as four 16-point DFTs (k1 = 4 q + r: x[n1] W64^{n1 r} then DFT16
-// over n1), the live NL inputs pruned statically.  Stage B: thread t owns
-// the window bins k = b0 + t + 64 o (column k1 = k mod 64): per 16-row slice
-// of its column one 4-point DFT, then a 16-term Horner chain per bin (see
-// rc4096_bins) and the demodulation.  The bins of one warp are contiguous
+//     A_{n2}[k1] = sum_{n1 < NL} x[64 n1 + n2] W_KC^{n1 k1}
+// (W = e^{+2 pi i / N}).  Stage A: thread n2 forms its column's KC
+// outputs as four (KC/4)-point DFTs (k1 = 4 q + r: x[n1] W_KC^{n1 r} then a
+// DFT over n1), the live NL inputs pruned statically.  Stage B: thread t
+// owns the window bins k = b0 + t + 64 o (column k1 = k mod KC): per
+// 16-row slice of its column one 4-point (N = 4096) or 2-point (2048) DFT,
+// then a 16-term Horner chain per bin (see rc_split_bins) and the
+// demodulation.  The bins of one warp are contiguous
 // (coalesced stores) and their count is warp-uniform when the window is a
 // multiple of 32 bins.  One 64-thread CTA per row, 6 per SM; per row 32 KB
 // of smem written and read once (the Stockham kernel moves 64 KB) and ~100k
@@ -366,20 +367,23 @@ constexpr int RC64_LD = 65;  // padded column stride: stage B's column reads are
 // stage B for one thread with C bins k = kb + 64 o, kb = b0 + t, o < C
 // (those at or past b0 + w are computed and dropped -- only in the warp
 // holding the window's ragged end).  With n2 = 16 a + b (a < 4, b < 16):
-//     X[k] = sum_b z^b Z_b[o mod 4],  z = W^k,
-//     Z_b[s] = sum_a (A_{16a+b}[k1] W^{16 a kb}) i^{a s}
-// since W^{16 a k} = W^{16 a kb} i^{a o}: per b one 4-point DFT (three
-// twiddles tau_a = W^{16 a kb}, per-thread constants) feeds every bin's
-// 16-term Horner chain.  d0 = the demodulation of bin kb; the other bins
-// follow by the constant steps W^{64 o} = W64^o and e^{j a dt 64 o}.
-template <int C>
-__device__ __forceinline__ void rc4096_bins(const float2 *__restrict__ col, const Rc64Roots &roots,
-                                            float2 z0, float2 tau1, float2 tau2, float2 tau3,
-                                            float2 d0, float2 *__restrict__ dst, int t, int w) {
+//     X[k] = sum_b z^b Z_b[o mod S],  z = W^k,
+//     Z_b[s] = sum_a (A_{16a+b}[k1] W^{16 a kb}) e^{2 pi i a s / S}
+// since W^{16 a k} = W^{16 a kb} W^{1024 a o} and W^{1024} = e^{2 pi i / S},
+// S = N / 1024 (4 at N = 4096: a 4-point DFT; 2 at N = 2048: sums and
+// differences): per b one small DFT (three twiddles tau_a = W^{16 a kb},
+// per-thread constants) feeds every bin's 16-term Horner chain.  d0 = the
+// demodulation of bin kb; the other bins follow by the constant steps
+// W^{64 o} = W64^{(4096 / N) o} and e^{j a dt 64 o}.
+template <int LOGN, int C>
+__device__ __forceinline__ void rc_split_bins(const float2 *__restrict__ col, const Rc64Roots &roots,
+                                              float2 z0, float2 tau1, float2 tau2, float2 tau3,
+                                              float2 d0, float2 *__restrict__ dst, int t, int w) {
+    constexpr int S = (1 << LOGN) / 1024, ZS = 4096 >> LOGN;
     f2x z[C], iz[C], acc[C];
 #pragma unroll
     for (int o = 0; o < C; ++o) {
-        const float2 zf = o == 0 ? z0 : cmul_p(z0, as_x(roots.w[o]), as_x(roots.iw[o]));
+        const float2 zf = o == 0 ? z0 : cmul_p(z0, as_x(roots.w[ZS * o]), as_x(roots.iw[ZS * o]));
         z[o] = as_x(zf);
         iz[o] = pk2(-zf.y, zf.x);
     }
@@ -390,11 +394,17 @@ __device__ __forceinline__ void rc4096_bins(const float2 *__restrict__ col, cons
     for (int b = 15; b >= 0; --b) {
         float2 u[4] = {col[b], cmul_p(col[16 + b], t1, it1), cmul_p(col[32 + b], t2, it2),
                        cmul_p(col[48 + b], t3, it3)};
-        idft<4, 4>(u);
+        if constexpr (S == 4) {
+            idft<4, 4>(u);
+        } else {
+            const float2 e = cadd(u[0], u[2]), f = cadd(u[1], u[3]);
+            u[0] = cadd(e, f);
+            u[1] = csub(e, f);
+        }
 #pragma unroll
         for (int o = 0; o < C; ++o)
-            acc[o] = b == 15 ? as_x(u[o & 3])
-                             : fma2(bc2(hi2(acc[o])), iz[o], fma2(bc2(lo2(acc[o])), z[o], as_x(u[o & 3])));
+            acc[o] = b == 15 ? as_x(u[o % S])
+                             : fma2(bc2(hi2(acc[o])), iz[o], fma2(bc2(lo2(acc[o])), z[o], as_x(u[o % S])));
     }
 #pragma unroll
     for (int o = 0; o < C; ++o) {
@@ -408,16 +418,27 @@ __device__ __forceinline__ void rc4096_bins(const float2 *__restrict__ col, cons
 #ifndef RC4096_PREFETCH
 #define RC4096_PREFETCH 2048  // rows ahead (~2 waves of 6 x 148 CTAs)
 #endif
-#ifndef RC4096_MINB
-#define RC4096_MINB 6  // CTAs per SM: 6 x 33 KB of smem
-#endif
-template <int NL, int CMAX>
-__global__ void __launch_bounds__(64, RC4096_MINB)
-range_compress_4096_kernel(const float2 *__restrict__ cube, int64_t n_el, const float2 *__restrict__ wk,
-                           const float2 *__restrict__ demod,
-                           const __grid_constant__ Rc64Roots roots, float2 *__restrict__ out,
-                           int gate_b0, int gate_w) {
-    __shared__ float2 cols[64 * RC64_LD];
+
+// N = 2^LOGN in {2048, 4096}: KC = N / 64 columns entries k1 per stage-A
+// column (stage-A DFT of KC / 4 points per k1 residue r), NL live samples
+// per column (n_f / 64).  Stage-A smem tile KC x 65 float2 (33 KB at 4096,
+// 17 KB at 2048).
+template <int LOGN>
+struct RcSplit {
+    static constexpr int N = 1 << LOGN, KC = N / 64, R = KC / 4;
+    static constexpr int MINB = LOGN == 12 ? 6 : 8;  // CTAs per SM
+};
+
+template <int LOGN, int NL, int CMAX>
+__global__ void __launch_bounds__(64, RcSplit<LOGN>::MINB)
+range_compress_split_kernel(const float2 *__restrict__ cube, int64_t n_el,
+                            const float2 *__restrict__ wk, const float2 *__restrict__ demod,
+                            const __grid_constant__ Rc64Roots roots, float2 *__restrict__ out,
+                            int gate_b0, int gate_w) {
+    using SP = RcSplit<LOGN>;
+    constexpr int N = SP::N, KC = SP::KC, R = SP::R;
+    static_assert(NL <= R, "live samples per column must fit the stage-A DFT");
+    __shared__ float2 cols[KC * RC64_LD];
     const int t = threadIdx.x;
     const int64_t row = blockIdx.x;
     const float2 *src = cube + row * (64 * NL);
@@ -431,47 +452,48 @@ range_compress_4096_kernel(const float2 *__restrict__ cube, int64_t n_el, const 
     // stage B's per-thread constants (the same for every row: L1/L2 hits),
     // fetched now so their latency hides behind stage A
     const int kb = gate_b0 + t;
-    const float2 z0 = __ldg(wk + (kb & 4095)), d0 = __ldg(demod + (kb < 4096 ? kb : 4095));
-    const float2 tau1 = __ldg(wk + ((16 * kb) & 4095)), tau2 = __ldg(wk + ((32 * kb) & 4095)),
-                 tau3 = __ldg(wk + ((48 * kb) & 4095));
+    const float2 z0 = __ldg(wk + (kb & (N - 1))), d0 = __ldg(demod + (kb < N ? kb : N - 1));
+    const float2 tau1 = __ldg(wk + ((16 * kb) & (N - 1))), tau2 = __ldg(wk + ((32 * kb) & (N - 1))),
+                 tau3 = __ldg(wk + ((48 * kb) & (N - 1)));
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        float2 v[16];
+        float2 v[R];
 #pragma unroll
         for (int n1 = 0; n1 < NL; ++n1)
-            v[n1] = (r == 0 || n1 == 0)
-                        ? x[n1]
-                        : cmul_p(x[n1], as_x(roots.w[n1 * r]), as_x(roots.iw[n1 * r]));
-        idft<16, NL>(v);
+            v[n1] = (r == 0 || n1 == 0) ? x[n1]
+                                        : cmul_p(x[n1], as_x(roots.w[(64 / KC) * n1 * r]),
+                                                 as_x(roots.iw[(64 / KC) * n1 * r]));
+        idft<R, NL>(v);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) cols[(4 * q + r) * RC64_LD + t] = v[q];
+        for (int q = 0; q < R; ++q) cols[(4 * q + r) * RC64_LD + t] = v[q];
     }
     __syncthreads();
     // bins per thread, uniform over the warp (max over its lanes)
     const int cw = (gate_w - (t & ~31) + 63) >> 6;
-    const float2 *col = cols + (kb & 63) * RC64_LD;
+    const float2 *col = cols + (kb & (KC - 1)) * RC64_LD;
     float2 *dst = out + row * gate_w;
     if (cw == CMAX) {
-        rc4096_bins<CMAX>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
+        rc_split_bins<LOGN, CMAX>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
     } else if constexpr (CMAX > 1) {
-        if (cw == CMAX - 1) rc4096_bins<CMAX - 1>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
+        if (cw == CMAX - 1)
+            rc_split_bins<LOGN, CMAX - 1>(col, roots, z0, tau1, tau2, tau3, d0, dst, t, gate_w);
     }
 }
 
-// W^k = e^{+2 pi i k / 4096} from float64
-__global__ void rc_wk_kernel(float2 *__restrict__ wk) {
+// W^k = e^{+2 pi i k / n}, k < n, from float64
+__global__ void rc_wk_kernel(float2 *__restrict__ wk, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 4096) return;
+    if (i >= n) return;
     double sn, cs;
-    sincospi((double)i / 2048.0, &sn, &cs);
+    sincospi(2.0 * (double)i / (double)n, &sn, &cs);
     wk[i] = make_float2((float)cs, (float)sn);
 }
 
-template <int NL, int C>
-int launch_rc4096_c(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
-                    const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
-    auto kern = range_compress_4096_kernel<NL, C>;
-    // smem-heavy (6 CTAs of 33 KB per SM): ask for the full carveout
+template <int LOGN, int NL, int C>
+int launch_rc_split_c(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
+                      const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
+    auto kern = range_compress_split_kernel<LOGN, NL, C>;
+    // smem-heavy: ask for the full carveout
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     for (int64_t r0 = 0; r0 < n_el; r0 += 2147483647ll) {
@@ -479,25 +501,29 @@ int launch_rc4096_c(const float2 *cube, int64_t n_el, const float2 *wk, const fl
         kern<<<(unsigned)nb, 64, 0, s>>>(cube + r0 * (64 * NL), n_el - r0, wk, demod, roots,
                                          out + r0 * (int64_t)gate_w, gate_b0, gate_w);
     }
-    return check_launch("range_compress_4096_kernel");
+    return check_launch("range_compress_split_kernel");
 }
 
-// bins per stage-B thread: C = ceil(w / 64) <= RC4096_MAX_C
-constexpr int RC4096_MAX_C = 8;
+// bins per stage-B thread: C = ceil(w / 64) <= RC_SPLIT_MAX_C
+constexpr int RC_SPLIT_MAX_C = 8;
 
-template <int NL>
-int launch_rc4096(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
-                  const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
+template <int LOGN, int NL>
+int launch_rc_split(const float2 *cube, int64_t n_el, const float2 *wk, const float2 *demod,
+                    const Rc64Roots &roots, float2 *out, int gate_b0, int gate_w, cudaStream_t s) {
+#define HHSAR_RC_SPLIT_CASE(c)                                                                  \
+    case c:                                                                                     \
+        return launch_rc_split_c<LOGN, NL, c>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
     switch ((gate_w + 63) / 64) {
-        case 1: return launch_rc4096_c<NL, 1>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 2: return launch_rc4096_c<NL, 2>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 3: return launch_rc4096_c<NL, 3>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 4: return launch_rc4096_c<NL, 4>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 5: return launch_rc4096_c<NL, 5>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 6: return launch_rc4096_c<NL, 6>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        case 7: return launch_rc4096_c<NL, 7>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
-        default: return launch_rc4096_c<NL, 8>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
+        HHSAR_RC_SPLIT_CASE(1)
+        HHSAR_RC_SPLIT_CASE(2)
+        HHSAR_RC_SPLIT_CASE(3)
+        HHSAR_RC_SPLIT_CASE(4)
+        HHSAR_RC_SPLIT_CASE(5)
+        HHSAR_RC_SPLIT_CASE(6)
+        HHSAR_RC_SPLIT_CASE(7)
+        default: return launch_rc_split_c<LOGN, NL, 8>(cube, n_el, wk, demod, roots, out, gate_b0, gate_w, s);
     }
+#undef HHSAR_RC_SPLIT_CASE
 }
 
 template <int LOGN>
@@ -666,9 +692,11 @@ extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64
     auto o = reinterpret_cast<float2 *>(out);
     int rc = HHSAR_OK;
 #ifndef HHSAR_RC_STOCKHAM_ONLY
-    if (n_t == 4096 && (n_f == 1024 || n_f == 512) && w <= 64 * RC4096_MAX_C) {
+    const bool split4096 = n_t == 4096 && (n_f == 1024 || n_f == 512);
+    const bool split2048 = n_t == 2048 && (n_f == 512 || n_f == 256);
+    if ((split4096 || split2048) && w <= 64 * RC_SPLIT_MAX_C) {
         float2 *wk = tables + 2 * n_t;
-        rc_wk_kernel<<<16, 256, 0, s>>>(wk);
+        rc_wk_kernel<<<(unsigned)((n_t + 255) / 256), 256, 0, s>>>(wk, (int)n_t);
         Rc64Roots roots;
         for (int m = 0; m < 64; ++m) {
             const double ph = 2.0 * M_PI * (double)m / 64.0;
@@ -680,8 +708,13 @@ extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64
             const double red = 2.0 * M_PI * (rev - nearbyint(rev));
             roots.dstep[o] = make_float2((float)cos(red), (float)sin(red));
         }
-        rc = n_f == 1024 ? launch_rc4096<16>(c, n_el, wk, demod_tab, roots, o, (int)b0, (int)w, s)
-                         : launch_rc4096<8>(c, n_el, wk, demod_tab, roots, o, (int)b0, (int)w, s);
+        const int gb = (int)b0, gw = (int)w;
+        if (split4096)
+            rc = n_f == 1024 ? launch_rc_split<12, 16>(c, n_el, wk, demod_tab, roots, o, gb, gw, s)
+                             : launch_rc_split<12, 8>(c, n_el, wk, demod_tab, roots, o, gb, gw, s);
+        else
+            rc = n_f == 512 ? launch_rc_split<11, 8>(c, n_el, wk, demod_tab, roots, o, gb, gw, s)
+                            : launch_rc_split<11, 4>(c, n_el, wk, demod_tab, roots, o, gb, gw, s);
         cudaFreeAsync(tables, s);
         return rc;
     }

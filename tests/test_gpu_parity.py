@@ -333,7 +333,10 @@ def test_config3_full_scale_vs_oracle(hh):
                                                     (300, 1024, 4, 0, 512), (300, 1024, 4, 3584, 512),
                                                     (70, 1024, 4, 4095, 1), (70, 1024, 4, 63, 65),
                                                     (70, 1024, 4, 1000, 449), (70, 512, 8, 49, 288),
-                                                    (70, 512, 8, 3000, 1096)])
+                                                    (70, 512, 8, 3000, 1096),
+                                                    # 2048-bin rows (config 3): the same split
+                                                    (70, 512, 4, 1600, 448), (70, 512, 4, 2047, 1),
+                                                    (70, 256, 8, 100, 300), (70, 512, 4, 31, 65)])
 def test_range_compress_window_equals_full_slice(n_el, n_f, upsample, b0, w):
     """The range-gated compression (only bins [b0, b0 + w) computed in the
     last pass and stored) against the same bins of the full compression."""

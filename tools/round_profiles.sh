@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
     --log-file $out/launches.csv python bench.py $args > $out/launches.log 2>&1
 python tools/step_once.py 4 > /dev/null 2>&1 && \
   ncu --set full --import-source on --clock-control none \
-      -k regex:"range_compress_4096_kernel|range_compress_kernel|leaf_points|merge_cartesian|grid_newton_kernel|grid_newton_fixup" -s 6 -c 6 \
+      -k regex:"range_compress_split_kernel|range_compress_kernel|leaf_points|merge_cartesian|grid_newton_kernel|grid_newton_fixup" -s 6 -c 6 \
       -o $out/config4 python tools/step_once.py 4 > $out/config4.log 2>&1
 python tools/profile_step.py --config 1 > /dev/null 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:bpa_tile -s 1 -c 1 \
