@@ -415,11 +415,11 @@ __device__ __forceinline__ void rc_split_bins(const float2 *__restrict__ col, co
     }
 }
 
-#ifndef RC4096_PREFETCH
-#define RC4096_PREFETCH 2048  // rows ahead (~2 waves of 6 x 148 CTAs)
+#ifndef RC_SPLIT_PREFETCH
+#define RC_SPLIT_PREFETCH 2048  // rows ahead (~2 waves of 6 x 148 CTAs)
 #endif
 
-// N = 2^LOGN in {2048, 4096}: KC = N / 64 columns entries k1 per stage-A
+// N = 2^LOGN in {2048, 4096}: KC = N / 64 entries k1 per stage-A
 // column (stage-A DFT of KC / 4 points per k1 residue r), NL live samples
 // per column (n_f / 64).  Stage-A smem tile KC x 65 float2 (33 KB at 4096,
 // 17 KB at 2048).
@@ -446,8 +446,8 @@ range_compress_split_kernel(const float2 *__restrict__ cube, int64_t n_el,
 #pragma unroll
     for (int n1 = 0; n1 < NL; ++n1) x[n1] = __ldcs(src + 64 * n1 + t);
     // pull a later CTA's row into L2 (one bulk prefetch)
-    if (t == 0 && row + RC4096_PREFETCH < n_el)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + RC4096_PREFETCH * (64 * NL)),
+    if (t == 0 && row + RC_SPLIT_PREFETCH < n_el)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + RC_SPLIT_PREFETCH * (64 * NL)),
                      "r"(64 * NL * 8) : "memory");
     // stage B's per-thread constants (the same for every row: L1/L2 hits),
     // fetched now so their latency hides behind stage A
