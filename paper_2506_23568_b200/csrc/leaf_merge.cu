@@ -610,8 +610,15 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
             const float fn = cf - bn;
             const float2 smp = kp ? gather_child_pairs<KERNEL>(kp, C, iu, iv, iw, fu, fv, fn)
                                   : gather_child<KERNEL>(kv, C, iu, iv, iw, fu, fv, fn);
+#ifdef HHSAR_LANDING_REDUCE
             const float nr = fmaf(ph, 0.15915494f, 12582912.0f) - 12582912.0f;
             const float red = fmaf(nr, 1.7484555e-7f, fmaf(nr, -6.28318548f, ph));
+#else
+            // |ph| <= pi + |phase change over half a block| (a few to ~20
+            // rad): the SFU's own reduction (x / 2 pi rounded once) costs
+            // <= |ph| 2^-24 ~ 1e-6 rad here
+            const float red = ph;
+#endif
             float sn, cs;
             __sincosf(red, &sn, &cs);
             cfma(acc[j], smp, make_float2(cs, sn));
