@@ -597,6 +597,10 @@ def rc_roofline(w, run, rc_ms, step_ms):
                            "peak_tflops": round(fp32 / 1e12, 1),
                            "frac": round(flops / (kms / 1e3) / fp32, 3)}
     out["traffic"] = _traffic(kname + "_config4")  # profiles/traffic.json
+    if split:
+        # what actually limits it (profiles/r02_config4_ncu.txt): the FP32
+        # pipe, not HBM -- the contract's bound field has no FP32 option
+        out["limiter"] = "FP32 FMA pipe (ncu: 75% busy alone; ~101k lane ops per row)"
     return out
 
 
