@@ -44,8 +44,12 @@ __device__ __forceinline__ int newton_iteration(const NewtonGeom &G, double tu, 
                                                 double tol, double max_step2, double max_step,
                                                 double z_floor) {
     const double xmn = G.ext[0], xmx = G.ext[1], ymn = G.ext[2], ymx = G.ext[3];
-    const double x0 = fmin(fmax(x, xmn), xmx);
-    const double y0 = fmin(fmax(y, ymn), ymx);
+    // clamps, zero test and convergence test written with comparisons: the
+    // float64 fmin / fmax of sm_100 cost ~8 instructions each (DSETP.MIN +
+    // NaN-handling selects), ~40% of an iteration in this form.  Results are
+    // those of fmin / fmax (NaN operands ignored) for every input.
+    const double xc = x > xmn ? x : xmn, yc = y > ymn ? y : ymn;  // fmax(x, lo): NaN -> lo
+    const double x0 = xc < xmx ? xc : xmx, y0 = yc < ymx ? yc : ymx;
     const double z2 = z * z;
     const double ax = x - xmn, bx = x - xmx, ay = y - ymn, by = y - ymx;
     const double yd = y - y0, xd = x - x0;
@@ -55,8 +59,9 @@ __device__ __forceinline__ int newton_iteration(const NewtonGeom &G, double tu, 
     const double a_v1 = xx + ay2 + z2, a_v2 = xx + by2 + z2;
     const double a_e1 = ax2 + ay2 + z2, a_e2 = ax2 + by2 + z2;
     const double a_e3 = bx2 + ay2 + z2, a_e4 = bx2 + by2 + z2;
-    if (fmin(fmin(fmin(a_u1, a_u2), fmin(a_v1, a_v2)), fmin(fmin(a_e1, a_e2), fmin(a_e3, a_e4))) ==
-        0.0)
+    // fmin over the eight == 0  <=>  some (non-NaN) value == 0
+    if ((a_u1 == 0.0) | (a_u2 == 0.0) | (a_v1 == 0.0) | (a_v2 == 0.0) | (a_e1 == 0.0) |
+        (a_e2 == 0.0) | (a_e3 == 0.0) | (a_e4 == 0.0))
         return 2;
     const double i1 = rsqrt_d(a_u1), i2 = rsqrt_d(a_u2), i3 = rsqrt_d(a_v1), i4 = rsqrt_d(a_v2);
     const double f1 = rsqrt_d(a_e1), f2 = rsqrt_d(a_e2), f3 = rsqrt_d(a_e3), f4 = rsqrt_d(a_e4);
@@ -68,7 +73,11 @@ __device__ __forceinline__ int newton_iteration(const NewtonGeom &G, double tu, 
     const double ru = G.c_uv * (a_u1 * i1 - a_u2 * i2) - tu;
     const double rv = G.c_uv * (a_v1 * i3 - a_v2 * i4) - tv;
     const double rn = G.c_nhi * sq - G.c_nlo * r - tn;
-    if (fmax(fabs(ru), fmax(fabs(rv), fabs(rn))) <= tol) return 1;
+    // fmax(|ru|, |rv|, |rn|) <= tol with fmax's NaN rule (a NaN operand is
+    // ignored; all three NaN -> NaN -> false)
+    if (!(fabs(ru) > tol) & !(fabs(rv) > tol) & !(fabs(rn) > tol) &
+        !((ru != ru) & (rv != rv) & (rn != rn)))
+        return 1;
     const double ja = G.c_uv * (ax * i1 - bx * i2);
     const double jb = G.c_uv * (yd * (i1 - i2));
     const double jc = G.c_uv * (z * (i1 - i2));
