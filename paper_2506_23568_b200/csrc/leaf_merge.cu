@@ -508,7 +508,8 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
         const double S0 = U0 * w, S1 = U1 * hw, S2 = fma(-S1, S1, U2) * hw;
         const double S3 = fma(-2.0 * S1, S2, U3) * hw, S4 = (U4 - 2.0 * S1 * S3 - S2 * S2) * hw;
         const double cn0 = (fma(g.c_nhi, S0, -g.c_nlo * R0) - C.o_n) * inv_step;
-        const double I0d = fmin(fmax(floor(cn0), -1048576.0), 1048576.0);
+        const double fl0 = floor(cn0);  // clamped to +-2^20 (comparisons: cheaper than fmin/fmax)
+        const double I0d = fl0 > -1048576.0 ? (fl0 < 1048576.0 ? fl0 : 1048576.0) : -1048576.0;
         const int I0 = (int)I0d;
         const float f0 = (float)(cn0 - I0d);
         const float n1 = (float)(fma(g.c_nhi, S1, -g.c_nlo * R1) * inv_step * sz);
