@@ -453,8 +453,9 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
     int64_t row;  // column (ix, iy)
     int k;        // z block
     if (tile) {
-        // a warp takes 4 adjacent columns x 8 adjacent z blocks: its lanes'
-        // taps share lattice rows and lines (the launcher checks alignment)
+        // a warp takes TC adjacent columns x 32 / TC adjacent z blocks (16 x
+        // 2): its lanes' taps share lattice rows and lines (the launcher
+        // checks the alignment)
         constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1, TK = 32 / TC;
         const int64_t w = qi >> 5;
         const int lane = (int)(qi & 31), kt_per = nzq / TK;
