@@ -169,16 +169,25 @@ __device__ __forceinline__ float2 gather_child(const float2 *__restrict__ vals, 
     return acc;
 }
 
+// one pair-staged stencil row: base + 16 idx as a single wide multiply-add
+__device__ __forceinline__ const float4 *pair_row(const float4 *base, unsigned idx) {
+    const float4 *p;
+    asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(p) : "r"(idx), "l"(base));
+    return p;
+}
+
 // The same gather from the pair-staged copy of the child lattices: entry i
 // holds (v[i], v[i + 1] - v[i]) in 16 B, so each lattice row of the stencil
 // is one 128-bit load (linear: 4 per sample instead of 8; cubic: 32 instead
-// of 64).
+// of 64).  ``base`` = the pair copy + the child's pool offset, formed once
+// per child by the caller; each row address is then pair_row (left to
+// itself the compiler re-derives the 64-bit (offset + index) * 16 + pairs
+// in four instructions per row).
 template <int KERNEL>
-__device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ pairs,
+__device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ base,
                                                      const MergeChild &C, int iu, int iv, int iw,
                                                      float fu, float fv, float fn) {
     const int su = C.nv * C.nn;
-    const float4 *base = pairs + C.offset;
     if (KERNEL == 0) {
         const unsigned i00 = (unsigned)((iu * C.nv + iv) * C.nn + iw);
         const unsigned idx[2][2] = {{i00, i00 + (unsigned)C.nn},
@@ -188,7 +197,7 @@ __device__ __forceinline__ float2 gather_child_pairs(const float4 *__restrict__ 
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int bb = 0; bb < 2; ++bb) {
-                const float4 v = __ldg(base + idx[a][bb]);  // (v[i], v[i+1] - v[i])
+                const float4 v = __ldg(pair_row(base, idx[a][bb]));  // (v[i], v[i+1] - v[i])
                 r[a][bb] = fma2(bc2(fn), pk2(v.z, v.w), pk2(v.x, v.y));
             }
         const f2x s0 = fma2(bc2(fv), sub2(r[0][1], r[0][0]), r[0][0]);
@@ -484,6 +493,7 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
     constexpr int lo = KERNEL ? 1 : 0;
     for (int c = 0; c < nk; ++c) {
         const MergeChild C = load_child(kids + c);
+        const float4 *kpc = kp ? kp + C.offset : nullptr;  // this child's pair rows
         // ---- n coordinate and phase: float64 series of r and sq at z_c
         const double ax = x - C.ext[0], bx = x - C.ext[1], ay = y - C.ext[2], by = y - C.ext[3];
         const double ss[4] = {fma(ax, ax, ay * ay), fma(ax, ax, by * by), fma(bx, bx, ay * ay),
@@ -610,7 +620,7 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
             bn = fminf(bn, n_base_hi);                              // top edge: base hi, fraction 1
             const int iw = I0 + (int)bn;
             const float fn = cf - bn;
-            const float2 smp = kp ? gather_child_pairs<KERNEL>(kp, C, iu, iv, iw, fu, fv, fn)
+            const float2 smp = kp ? gather_child_pairs<KERNEL>(kpc, C, iu, iv, iw, fu, fv, fn)
                                   : gather_child<KERNEL>(kv, C, iu, iv, iw, fu, fv, fn);
 #ifdef HHSAR_LANDING_REDUCE
             const float nr = fmaf(ph, 0.15915494f, 12582912.0f) - 12582912.0f;
