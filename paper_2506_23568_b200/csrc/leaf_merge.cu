@@ -456,27 +456,29 @@ merge_cartesian_series_kernel(double ox, double oy, double oz, double sx, double
                               const float2 *__restrict__ kv, const float4 *__restrict__ kp,
                               hhsar_geom g, float2 *__restrict__ out,
                               int64_t *__restrict__ flagged, int tile) {
-    const int64_t qi = (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
-    if (qi >= nq) return;
-    const int nzq = (nz + ZQ - 1) / ZQ;
-    int64_t row;  // column (ix, iy)
-    int k;        // z block
+    int64_t row;  // column (ix, iy) = ix * ny + iy
+    int k, ix, iy;  // z block, column
     if (tile) {
-        // a warp takes TC adjacent columns x 32 / TC adjacent z blocks (16 x
-        // 2): its lanes' taps share lattice rows and lines (the launcher
-        // checks the alignment)
+        // whole volume, 3-D grid (ny / TC, nzq / (4 TK), nx): a warp takes
+        // TC adjacent columns x TK = 32 / TC adjacent z blocks (16 x 2) --
+        // its lanes' taps share lattice rows and lines -- and a CTA's four
+        // warps take adjacent z-block tiles; no integer division anywhere
         constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1, TK = 32 / TC;
-        const int64_t w = qi >> 5;
-        const int lane = (int)(qi & 31), kt_per = nzq / TK;
-        const int64_t rg = w / kt_per;
-        row = q0 / nzq + rg * TC + lane / TK;
-        k = (int)(w - rg * kt_per) * TK + lane % TK;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        ix = blockIdx.z;
+        iy = blockIdx.x * TC + lane / TK;
+        k = (blockIdx.y * (MERGE_THREADS / 32) + warp) * TK + lane % TK;
+        row = (int64_t)ix * ny + iy;
     } else {
+        const int64_t qi = (int64_t)blockIdx.x * MERGE_THREADS + threadIdx.x;
+        if (qi >= nq) return;
+        const int nzq = (nz + ZQ - 1) / ZQ;
         const int64_t Q = q0 + qi;
         row = Q / nzq;
         k = (int)(Q - row * nzq);
+        iy = (int)(row % ny);
+        ix = (int)(row / ny);
     }
-    const int iy = (int)(row % ny), ix = (int)(row / ny);
     const double x = __dadd_rn(ox, __dmul_rn(sx, (double)ix));
     const double y = __dadd_rn(oy, __dmul_rn(sy, (double)iy));
     const float xf = (float)x, yf = (float)y;
@@ -832,14 +834,19 @@ extern "C" int hhsar_merge_cartesian(const double *origin, const double *step, c
             const int64_t nzq = (dims[2] + zq - 1) / zq;
             const int64_t q0 = (vox_begin / dims[2]) * nzq + (vox_begin % dims[2]) / zq;
             const int64_t q1 = ((vox_end - 1) / dims[2]) * nzq + ((vox_end - 1) % dims[2]) / zq + 1;
-            const unsigned blocks = (unsigned)((q1 - q0 + MERGE_THREADS - 1) / MERGE_THREADS);
-            constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1;
-            const int tile = HHSAR_LANDING_TILE > 0 && nzq % (32 / TC) == 0 &&
-                             q0 % (TC * nzq) == 0 && (q1 - q0) % (TC * nzq) == 0;
-            kern<<<blocks, MERGE_THREADS, 0, s>>>(origin[0], origin[1], origin[2], step[0], step[1],
-                                                  step[2], (int)dims[1], (int)dims[2], vox_begin,
-                                                  vox_end, q0, q1 - q0, kids, (int)n_children, kv,
-                                                  kp, *geom, o, flagged, tile);
+            unsigned blocks = (unsigned)((q1 - q0 + MERGE_THREADS - 1) / MERGE_THREADS);
+            // warp tiles over the whole volume (3-D grid) when the shape allows
+            constexpr int TC = HHSAR_LANDING_TILE > 0 ? HHSAR_LANDING_TILE : 1, TK = 32 / TC;
+            constexpr int KT_CTA = TK * (MERGE_THREADS / 32);  // z blocks per CTA
+            const int tile = HHSAR_LANDING_TILE > 0 && vox_begin == 0 && vox_end == total &&
+                             dims[1] % TC == 0 && nzq % KT_CTA == 0 && dims[0] <= 65535 &&
+                             nzq / KT_CTA <= 65535;
+            dim3 grid(blocks);
+            if (tile) grid = dim3((unsigned)(dims[1] / TC), (unsigned)(nzq / KT_CTA), (unsigned)dims[0]);
+            kern<<<grid, MERGE_THREADS, 0, s>>>(origin[0], origin[1], origin[2], step[0], step[1],
+                                                step[2], (int)dims[1], (int)dims[2], vox_begin,
+                                                vox_end, q0, q1 - q0, kids, (int)n_children, kv, kp,
+                                                *geom, o, flagged, tile);
         };
         if (kernel == 0) {
             if (zq == 8) launch_s(merge_cartesian_series_kernel<0, 8>);
