@@ -503,7 +503,7 @@ def e2e_leg(args, w, params, cube, e0, e1, world, rank, dev):
         # timed region; uploads overlap the previous volume's tail and
         # copy-back (opposite link directions)
         from paper_2506_23568_b200 import ffbp
-        k = max(4, args.e2e_calls + 2)
+        k = max(8, args.e2e_calls + 2)  # the same pinned cube, k scans
         for _ in range(2):  # warm-up: pinned output pool, plan cache
             for vol in ffbp.hhffbpa_reconstruct_stream([data] * 3, w.region, w.dims, params,
                                                        upsample=w.upsample,
