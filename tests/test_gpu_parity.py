@@ -511,8 +511,12 @@ def test_sdc_phase_operator_vs_reference(hh, small):
     assert np.max(np.abs(got - want)) < 2e-6
 
 
-@pytest.mark.parametrize("config,kernel", [(2, "linear"), (3, "linear"), (2, "cubic")])
-def test_landing_series_equals_per_voxel(config, kernel):
+@pytest.mark.parametrize("config,kernel,dims", [(2, "linear", None), (3, "linear", None),
+                                                (2, "cubic", None),
+                                                # ragged: no warp tiles, partial z blocks
+                                                (2, "linear", (37, 29, 13)),
+                                                (2, "cubic", (21, 40, 7))])
+def test_landing_series_equals_per_voxel(config, kernel, dims):
     """The z-series landing (merge_cartesian_series_kernel: quartic Taylor
     polynomials per 8-voxel z run, pair-staged lattice gathers) against the
     per-voxel float64 landing (HHSAR_LANDING_PER_VOXEL) on the same device
@@ -526,7 +530,7 @@ def test_landing_series_equals_per_voxel(config, kernel):
                        generator=gen)
     el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
     params = ffbp.FfbpParams(levels=w.levels, kernel=kernel)
-    args = (cube, el, bpa.el_f32x4(el), w.freqs, w.region, w.dims, params, w.levels,
+    args = (cube, el, bpa.el_f32x4(el), w.freqs, w.region, dims or w.dims, params, w.levels,
             w.merge_factor, w.upsample)
     out = {}
     try:
