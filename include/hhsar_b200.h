@@ -208,11 +208,14 @@ int hhsar_grid_plan(hhsar_grid_desc *grids, int64_t n_grids, const double *leaf_
 /* Range gate of the leaf stage: gate[0] = b0, gate[1] = w (int64, device)
  * such that every delay bin a valid leaf point can read through
  * hhsar_leaf_bp lies in [b0, b0 + w) (w a multiple of 32 unless clipped at
- * n_t), from the plan's element and slack boxes of the n_leaves leaf grids
- * (device descs).  Feed it to hhsar_range_compress_window.  No reference
- * counterpart: the reference computes every bin (rangecomp.py:61-101). */
-int hhsar_leaf_range_gate(const hhsar_grid_desc *leaves, int64_t n_leaves, double dt,
-                          int64_t n_t, int64_t *gate, void *stream);
+ * n_t), from the plan's descriptors of the n_leaves leaf grids (device
+ * descs): the near-band n range of each leaf lattice bounds the vertex
+ * distance sum of its valid points, hence their distances to every leaf
+ * element.  geom: the plan's (host) geometry.  Feed it to
+ * hhsar_range_compress_window.  No reference counterpart: the reference
+ * computes every bin (rangecomp.py:61-101). */
+int hhsar_leaf_range_gate(const hhsar_grid_desc *leaves, int64_t n_leaves, const hhsar_geom *geom,
+                          double dt, int64_t n_t, int64_t *gate, void *stream);
 
 /* Newton inversion of every ACTIVE (u, v) column of every grid (desc.act_*
  * rectangle, at desc.col_offset in a work list of n_cols columns), warm

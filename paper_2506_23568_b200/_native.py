@@ -61,7 +61,7 @@ SIGNATURES = {
                                     ctypes.c_int),
     "hhsar_leaf_boxes": ([_P, _P, _I64, _P, _P], ctypes.c_int),
     "hhsar_grid_plan": ([_P, _I64, _P, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
-    "hhsar_leaf_range_gate": ([_P, _I64, _D, _I64, _P, _P], ctypes.c_int),
+    "hhsar_leaf_range_gate": ([_P, _I64, _P, _D, _I64, _P, _P], ctypes.c_int),
     "hhsar_grid_newton": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "hhsar_volume_dot": ([_P, _P, _I64, _I32, _P, _P], ctypes.c_int),
     "hhsar_volume_residual": ([_P, _P, _I64, _I32, _D, _D, _P, _P], ctypes.c_int),

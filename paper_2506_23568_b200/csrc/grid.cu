@@ -807,58 +807,71 @@ grid_offsets_kernel(hhsar_grid_desc *__restrict__ grids, int n, int64_t *__restr
 }
 
 // Delay-bin window [b0, b0 + w) the leaf stage can read (ffbp.leaf_range_gate
-// restated; same float64 operations, so the same integers): valid leaf points
-// lie in their grid's slack box and leaf elements in its element box, so
-// every leaf delay lies between the boxes' nearest and farthest distances;
-// the margin covers the leaf kernel's staging overhang (element-box
-// diagonal) plus interpolation / rounding pad.  One CTA.
+// restated; same float64 operations, so the same integers).  A valid leaf
+// point p lies on a near-band plane w in [near_lo, near_hi] (finish_plane,
+// the march ends at near_hi) where Newton converged to n(p) = origin_n +
+// step w within tol.  n = c_nhi sqrt(r^2 - gap) - c_nlo r is increasing in
+// the vertex distance sum r (dn/dr >= c_nhi - c_nlo > 0), with inverse
+//     r(n) = (c_nlo n + c_nhi sqrt(n^2 + (c_nhi^2 - c_nlo^2) gap)) / (c_nhi^2 - c_nlo^2),
+// so r(p) lies in [r(n_lo), r(n_hi)].  The four vertices v_i lie within
+// Dc of the element-box centre c, so |p - c| lies within r/4 -+ Dc, and the
+// leaf kernel's staging windows |p - c| -+ |e - c| (triangle inequality)
+// within r/4 -+ (Dc + hd), hd the half 3-D diagonal of the element box;
+// every delay it reads lies inside.  4 bins of pad each side cover the
+// kernel's +-2-bin windows, floors and fast-path tests.  (The plan's
+// containment boxes give a far looser bound: at config 4 valid leaf points
+// span 100 bins, the slack boxes 288.)  One CTA.
 __global__ void __launch_bounds__(SCAN_THREADS)
-leaf_gate_kernel(const hhsar_grid_desc *__restrict__ leaves, int n, double inv_bin, int64_t n_t,
-                 int64_t *__restrict__ gate) {
-    __shared__ double s_lo[SCAN_THREADS / 32], s_hi[SCAN_THREADS / 32], s_dg[SCAN_THREADS / 32];
-    double dmin = DBL_MAX, dmax = 0.0, diag = 0.0;
+leaf_gate_kernel(const hhsar_grid_desc *__restrict__ leaves, int n, hhsar_geom g, double inv_bin,
+                 int64_t n_t, int64_t *__restrict__ gate) {
+    __shared__ double s_lo[SCAN_THREADS / 32], s_hi[SCAN_THREADS / 32];
+    double dmin = DBL_MAX, dmax = 0.0;
+    const double A = xsub(xsq(g.c_nhi), xsq(g.c_nlo));
     for (int i = threadIdx.x; i < n; i += SCAN_THREADS) {
         const hhsar_grid_desc &D = leaves[i];
-        double g2 = 0.0, f2 = 0.0, d2 = 0.0;
+        const double gap = box_gap_exact(D.ext);
+        const double Ag = xmul(A, gap);
+        const double n_lo = xsub(xadd(D.origin[2], xmul(g.step, (double)D.near_lo[2])), g.tol);
+        const double n_hi = xadd(xadd(D.origin[2], xmul(g.step, (double)D.near_hi[2])), g.tol);
+        const double r_lo = xdiv(xadd(xmul(g.c_nlo, n_lo), xmul(g.c_nhi, xsqrt(xadd(xsq(n_lo), Ag)))), A);
+        const double r_hi = xdiv(xadd(xmul(g.c_nlo, n_hi), xmul(g.c_nhi, xsqrt(xadd(xsq(n_hi), Ag)))), A);
+        const double cx = xmul(0.5, xadd(D.box[0], D.box[3]));
+        const double cy = xmul(0.5, xadd(D.box[1], D.box[4]));
+        const double cz = xmul(0.5, xadd(D.box[2], D.box[5]));
+        const double z2 = xsq(cz);
+        double dc = 0.0;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double blo = D.box[a], bhi = D.box[3 + a], slo = D.slack_lo[a],
-                         shi = D.slack_hi[a];
-            const double gap = fmax(0.0, fmax(blo - shi, slo - bhi));
-            const double far = fmax(fabs(bhi - slo), fabs(shi - blo));
-            const double ext = bhi - blo;
-            // no FMA contraction: the same roundings as the numpy form
-            g2 = a ? __dadd_rn(g2, __dmul_rn(gap, gap)) : __dmul_rn(gap, gap);
-            f2 = a ? __dadd_rn(f2, __dmul_rn(far, far)) : __dmul_rn(far, far);
-            d2 = a ? __dadd_rn(d2, __dmul_rn(ext, ext)) : __dmul_rn(ext, ext);
+        for (int q = 0; q < 4; ++q) {
+            const double vx = D.ext[q >> 1], vy = D.ext[2 + (q & 1)];
+            dc = fmax(dc, xsqrt(xadd(xadd(xsq(xsub(cx, vx)), xsq(xsub(cy, vy))), z2)));
         }
-        dmin = fmin(dmin, sqrt(g2));
-        dmax = fmax(dmax, sqrt(f2));
-        diag = fmax(diag, sqrt(d2));
+        const double hd = xmul(0.5, xsqrt(xadd(xadd(xsq(xsub(D.box[3], D.box[0])),
+                                                   xsq(xsub(D.box[4], D.box[1]))),
+                                              xsq(xsub(D.box[5], D.box[2])))));
+        const double pad = xadd(dc, hd);
+        dmin = fmin(dmin, xsub(xmul(0.25, r_lo), pad));
+        dmax = fmax(dmax, xadd(xmul(0.25, r_hi), pad));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-        diag = fmax(diag, __shfl_xor_sync(0xffffffffu, diag, o));
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) {
         s_lo[wid] = dmin;
         s_hi[wid] = dmax;
-        s_dg[wid] = diag;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int k = 1; k < SCAN_THREADS / 32; ++k) {
             dmin = fmin(dmin, s_lo[k]);
             dmax = fmax(dmax, s_hi[k]);
-            diag = fmax(diag, s_dg[k]);
         }
-        const int64_t margin = (int64_t)ceil(__dmul_rn(diag, inv_bin)) + 6;
-        int64_t b0 = (int64_t)floor(__dmul_rn(dmin, inv_bin)) - margin;
+        dmin = dmin > 0.0 ? dmin : 0.0;
+        int64_t b0 = (int64_t)floor(xmul(dmin, inv_bin)) - 4;
         b0 = b0 > 0 ? b0 : 0;
-        int64_t b1 = (int64_t)ceil(__dmul_rn(dmax, inv_bin)) + margin + 1;
+        int64_t b1 = (int64_t)ceil(xmul(dmax, inv_bin)) + 5;
         b1 = b1 < n_t ? b1 : n_t;
         int64_t w = (b1 - b0 + 31) / 32 * 32;
         w = w < n_t - b0 ? w : n_t - b0;
@@ -867,12 +880,13 @@ leaf_gate_kernel(const hhsar_grid_desc *__restrict__ leaves, int n, double inv_b
     }
 }
 
-extern "C" int hhsar_leaf_range_gate(const hhsar_grid_desc *leaves, int64_t n_leaves, double dt,
-                                     int64_t n_t, int64_t *gate, void *stream) {
-    HHSAR_REQUIRE(n_leaves > 0 && n_leaves < (1ll << 31) && dt > 0.0 && n_t > 0,
+extern "C" int hhsar_leaf_range_gate(const hhsar_grid_desc *leaves, int64_t n_leaves,
+                                     const hhsar_geom *geom, double dt, int64_t n_t, int64_t *gate,
+                                     void *stream) {
+    HHSAR_REQUIRE(n_leaves > 0 && n_leaves < (1ll << 31) && geom != nullptr && dt > 0.0 && n_t > 0,
                   "leaf_range_gate: bad arguments");
     leaf_gate_kernel<<<1, SCAN_THREADS, 0, as_stream(stream)>>>(
-        leaves, (int)n_leaves, 2.0 / (HHSAR_C_LIGHT * dt), n_t, gate);
+        leaves, (int)n_leaves, *geom, 2.0 / (HHSAR_C_LIGHT * dt), n_t, gate);
     return check_launch("leaf_gate_kernel");
 }
 

@@ -173,11 +173,14 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
             const float xhi = (dmax + re) * k.inv_bin - k.x0;
             const int lo = max((int)floorf(xlo) - 2, 0);
             const int hi = min((int)floorf(xhi) + 2, k.n_t - 1);
-            // staged bins [lo', lo' + TW) with lo' + TW <= n_t - 1, so every
-            // staged bin has a successor (no clamps below); the window still
-            // covers every unit's base bin, with a bin of rounding margin
-            const int los = min(lo, k.n_t - 1 - TW);
-            const bool fast = xlo >= 1.f && xhi <= k.xmax - 2.f && hi - lo + 1 <= TW && los >= 0;
+            // staged bins [lo', lo' + TW) with lo' + TW <= n_t - 1 where the
+            // row is long enough, so every staged bin has a successor; the
+            // window still covers every unit's base bin, with a bin of
+            // rounding margin.  A (range-gated) row shorter than TW + 1 bins
+            // is staged from bin 0, bins past n_t - 2 clamped below: no unit
+            // reads them (its base bin is <= xhi <= n_t - 3).
+            const int los = max(0, min(lo, k.n_t - 1 - TW));
+            const bool fast = xlo >= 1.f && xhi <= k.xmax - 2.f && hi - lo + 1 <= TW;
             const unsigned off = (unsigned)(t * TW - los) * 16u - LP_MAGIC_BITS * 16u;
             s_el[t] = make_float4(e.x, e.y, e.z, __int_as_float(fast ? (int)off : -1));
             s_lo[t] = fast ? los : -1;
@@ -190,7 +193,7 @@ leaf_points_kernel(const hhsar_grid_desc *__restrict__ grids, int chunks,
         for (int q = t; q < cn * TW; q += LPT) {
             const int j = q >> lw, lo = s_lo[j];
             if (lo < 0) continue;
-            const int bin = lo + (q & (TW - 1));
+            const int bin = min(lo + (q & (TW - 1)), k.n_t - 2);
             const float2 *row = env + (s_row[j] + bin);
             const float2 v0 = __ldg(row), v1 = __ldg(row + 1);
             const float2 r = __ldg(rot + bin);

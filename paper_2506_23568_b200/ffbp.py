@@ -315,7 +315,8 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
         a, b = sched.level_slices[0]
         _native.call("hhsar_leaf_range_gate",
                      ctypes.c_void_p(descs_dev.data_ptr() + a * _native.GRID_DTYPE.itemsize),
-                     b - a, float(gate_dt), int(gate_bins), _native.c_void_p_offset(status, 24),
+                     b - a, _native.ptr(geom), float(gate_dt), int(gate_bins),
+                     _native.c_void_p_offset(status, 24),
                      stream)
     if cached is not None:
         return dict(el_dev=el_dev, sched=sched, descs_dev=descs_dev, geom=geom,
@@ -537,31 +538,51 @@ NEWTON_FIRST_MAX_COLUMNS = 131072  # as the native NEWTON_SPEC2_MAX_COLS (grid.c
 
 def leaf_range_gate(lat, sched, dt: float, n_t: int) -> tuple[int, int]:
     """Delay-bin window [b0, b0 + w) that holds every delay the leaf stage can
-    read.  A valid leaf point lies in its grid's slack box (ffbp.py:282-289,
-    containment) and a leaf element in the grid's element box, so every
-    point-element distance is within [min, max] of the box-to-box distances;
-    the leaf kernel's staging windows (triangle inequality around the box
-    centre) can overhang that by the element box's diagonal, plus 2 bins of
-    interpolation/rounding pad on each side.  Only the leaf stage reads
-    envelopes (merges read lattices), so profiles outside the gate are never
-    needed: config 4 keeps 288 of 4,096 bins.  Host restatement of
-    hhsar_leaf_range_gate (the step uses the device one, which comes back
-    with the plan; tests check the two agree)."""
+    read.  A valid leaf point lies on a near-band plane w in [near_lo,
+    near_hi] of its lattice (ffbp.py:294-301: only the two rings nearest the
+    region's image carry values) where Newton converged to n = origin_n +
+    step w within tol (ffbp.py:271-282).  n = c_nhi sqrt(r^2 - gap) - c_nlo r
+    (spectrum.py:255-257) increases with the vertex distance sum r, so r lies
+    in [r(n_lo), r(n_hi)] with r(n) = (c_nlo n + c_nhi sqrt(n^2 + A gap)) / A,
+    A = c_nhi^2 - c_nlo^2; the four vertices lie within Dc of the element-box
+    centre c, so |p - c| lies within r/4 -+ Dc and the leaf kernel's staging
+    windows |p - c| -+ |e - c| within r/4 -+ (Dc + hd) (hd: half the element
+    box's 3-D diagonal), plus 4 bins of pad each side.  Only the leaf stage
+    reads envelopes (merges read lattices), so profiles outside the gate are
+    never needed: config 4 keeps 128 of 4,096 bins (the containment boxes
+    would keep 288).  Host restatement of hhsar_leaf_range_gate (the step
+    uses the device one, which comes back with the plan; tests check the
+    two agree: same float64 operations in the same order)."""
     d = lat.descs
+    g = lat.geom
     a, b = sched.level_slices[0]
+    ext = np.asarray(d["ext"][a:b], dtype=np.float64)
     box = np.asarray(d["box"][a:b], dtype=np.float64)
-    blo, bhi = box[:, :3], box[:, 3:]
-    slo = np.asarray(d["slack_lo"][a:b], dtype=np.float64)
-    shi = np.asarray(d["slack_hi"][a:b], dtype=np.float64)
-    gap = np.maximum(0.0, np.maximum(blo - shi, slo - bhi))
-    far = np.maximum(np.abs(bhi - slo), np.abs(shi - blo))
-    d_min = float(np.sqrt((gap * gap).sum(axis=1)).min())
-    d_max = float(np.sqrt((far * far).sum(axis=1)).max())
-    diag = float(np.sqrt(((bhi - blo) ** 2).sum(axis=1)).max())
+    origin_n = np.asarray(d["origin"][a:b, 2], dtype=np.float64)
+    near_lo = np.asarray(d["near_lo"][a:b, 2], dtype=np.float64)
+    near_hi = np.asarray(d["near_hi"][a:b, 2], dtype=np.float64)
+    c_nhi, c_nlo, step, tol = (float(g[k][0]) for k in ("c_nhi", "c_nlo", "step", "tol"))
+    A = c_nhi * c_nhi - c_nlo * c_nlo
+    gap = 4.0 * (ext[:, 1] - ext[:, 0]) ** 2 + 4.0 * (ext[:, 3] - ext[:, 2]) ** 2
+    Ag = A * gap
+    n_lo = (origin_n + step * near_lo) - tol
+    n_hi = (origin_n + step * near_hi) + tol
+    r_lo = (c_nlo * n_lo + c_nhi * np.sqrt(n_lo * n_lo + Ag)) / A
+    r_hi = (c_nlo * n_hi + c_nhi * np.sqrt(n_hi * n_hi + Ag)) / A
+    c = 0.5 * (box[:, :3] + box[:, 3:])
+    z2 = c[:, 2] * c[:, 2]
+    dc = np.zeros(b - a)
+    for q in range(4):
+        vx, vy = ext[:, q >> 1], ext[:, 2 + (q & 1)]
+        dc = np.maximum(dc, np.sqrt(((c[:, 0] - vx) ** 2 + (c[:, 1] - vy) ** 2) + z2))
+    e = box[:, 3:] - box[:, :3]
+    hd = 0.5 * np.sqrt((e[:, 0] ** 2 + e[:, 1] ** 2) + e[:, 2] ** 2)
+    pad = dc + hd
+    d_min = max(float((0.25 * r_lo - pad).min()), 0.0)
+    d_max = float((0.25 * r_hi + pad).max())
     inv_bin = 2.0 / (C_LIGHT * dt)
-    margin = int(np.ceil(diag * inv_bin)) + 6
-    b0 = max(0, int(np.floor(d_min * inv_bin)) - margin)
-    b1 = min(n_t, int(np.ceil(d_max * inv_bin)) + margin + 1)
+    b0 = max(0, int(np.floor(d_min * inv_bin)) - 4)
+    b1 = min(n_t, int(np.ceil(d_max * inv_bin)) + 5)
     w = min(n_t - b0, -(-(b1 - b0) // 32) * 32)
     return b0, w
 

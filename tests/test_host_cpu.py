@@ -208,32 +208,47 @@ def test_profile_cut_matches_reference():
 
 def test_leaf_range_gate_host_restatement():
     """ffbp.leaf_range_gate (the host restatement of hhsar_leaf_range_gate):
-    one leaf whose element box and slack box are unit-separated along z
-    gives the window of their nearest/farthest distances, widened by the
-    element-box diagonal and the 6-bin pad, rounded up to 32 bins and
-    clipped to the profile."""
+    points whose compressed n lies in a leaf's near band, seen from any
+    element of the leaf, fall inside the gate with the leaf kernel's fast-
+    path margins (>= 1 bin above b0, <= 3 bins below b0 + w - 1); the window
+    is a multiple of 32 bins and clipped at the profile end."""
     from types import SimpleNamespace
+    rng = np.random.default_rng(5)
+    k_min, k_max = 2 * np.pi * 77e9 / model.C_LIGHT, 2 * np.pi * 81e9 / model.C_LIGHT
+    c_nhi, c_nlo = k_max / (4 * np.pi), k_min / (4 * np.pi)
+    geom = _native.host_struct(_native.GEOM_DTYPE, dict(c_nhi=c_nhi, c_nlo=c_nlo,
+                                                         step=1 / 1.4, tol=1e-9))
+    ext = np.array([-0.01, 0.006, 0.002, 0.018])           # lateral element box
     descs = np.zeros(2, dtype=_native.GRID_DTYPE)
-    descs["box"][0] = [0.0, 0.0, 0.0, 0.01, 0.02, 0.0]       # elements: 1 x 2 cm at z = 0
-    descs["slack_lo"][0] = [-0.1, -0.1, 0.3]
-    descs["slack_hi"][0] = [0.1, 0.1, 0.4]
-    lat = SimpleNamespace(descs=descs)
+    descs["ext"][0] = ext
+    descs["box"][0] = [ext[0], ext[2], -0.004, ext[1], ext[3], 0.003]
+    descs["origin"][0] = [0.0, 0.0, 4.0]
+    descs["near_lo"][0] = [0, 0, 3]
+    descs["near_hi"][0] = [0, 0, 12]
+    lat = SimpleNamespace(descs=descs, geom=geom)
     sched = SimpleNamespace(level_slices=[(0, 1), (1, 2)])
-    c = model.C_LIGHT
-    dt = 2.0 * 0.005 / c                                    # 5 mm range bins
+    dt = 2.0 * 0.004 / model.C_LIGHT                       # 4 mm range bins
     b0, w = ffbp.leaf_range_gate(lat, sched, dt, 4096)
-    inv_bin = 2.0 / (c * dt)
-    d_min = 0.3
-    far = np.maximum(np.abs(np.array([0.01, 0.02, 0.0]) - np.array([-0.1, -0.1, 0.3])),
-                     np.abs(np.array([0.1, 0.1, 0.4]) - np.array([0.0, 0.0, 0.0])))
-    d_max = float(np.sqrt((far ** 2).sum()))
-    margin = int(np.ceil(np.sqrt(0.01 ** 2 + 0.02 ** 2) * inv_bin)) + 6
-    want_b0 = int(np.floor(d_min * inv_bin)) - margin
-    want_b1 = int(np.ceil(d_max * inv_bin)) + margin + 1
-    assert b0 == want_b0 and w % 32 == 0 and b0 + w >= want_b1 and w - (want_b1 - want_b0) < 32
+    assert w % 32 == 0 and 0 < b0 < 4096 - w
+    n_lo, n_hi = 4.0 + 3 / 1.4, 4.0 + 12 / 1.4
+    # random points above the array; keep those on the near band's n range
+    p = np.stack([rng.uniform(-0.4, 0.4, 400000), rng.uniform(-0.4, 0.4, 400000),
+                  rng.uniform(0.05, 0.6, 400000)], axis=1)
+    vs = np.array([[ext[i], ext[2 + j], 0.0] for i in (0, 1) for j in (0, 1)])
+    r = sum(np.linalg.norm(p - v, axis=1) for v in vs)
+    gap = 4 * (ext[1] - ext[0]) ** 2 + 4 * (ext[3] - ext[2]) ** 2
+    n = c_nhi * np.sqrt(r * r - gap) - c_nlo * r
+    p = p[(n >= n_lo) & (n <= n_hi)]
+    assert len(p) > 1000
+    e = np.stack([rng.uniform(ext[0], ext[1], 64), rng.uniform(ext[2], ext[3], 64),
+                  rng.uniform(-0.004, 0.003, 64)], axis=1)
+    bins = np.linalg.norm(p[:, None, :] - e[None, :, :], axis=2) * (2.0 / (model.C_LIGHT * dt))
+    assert bins.min() - b0 >= 1.0 and bins.max() - b0 <= w - 4.0
+    # tight: the near band's own delay span plus the pads, not the profile
+    assert w <= (bins.max() - bins.min()) + 64
     # clipped at the profile end
-    b0c, wc = ffbp.leaf_range_gate(lat, sched, dt, want_b1 - 5)
-    assert b0c == want_b0 and b0c + wc == want_b1 - 5
+    b0c, wc = ffbp.leaf_range_gate(lat, sched, dt, b0 + w - 7)
+    assert b0c == b0 and b0c + wc == b0 + w - 7
 
 
 def test_check_grids_reference_order():

@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 from paper_2506_23568_b200 import _native, rangecomp, workloads  # noqa: E402
 
-GATES = {3: (0, 352), 4: (49, 288), 1: (0, 1024)}
+GATES = {3: (10, 64), 4: (65, 128), 1: (0, 1024)}
 for cfg in [int(c) for c in (sys.argv[1:] or ["1", "3", "4"])]:
     w = workloads.config(cfg)
     gen = torch.Generator(device="cuda").manual_seed(1)
