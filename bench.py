@@ -600,7 +600,10 @@ def rc_roofline(w, run, rc_ms, step_ms):
     if split:
         # what actually limits it (profiles/r02_config4_ncu.txt): the FP32
         # pipe, not HBM -- the contract's bound field has no FP32 option
-        out["limiter"] = "FP32 FMA pipe (ncu: 75% busy alone; ~101k lane ops per row)"
+        c = -(-gw // 64)
+        lane_ops = (54.5 if n_t == 4096 else 27.0) * 1e3 + 64 * 16 * (28 + 4 * c)
+        out["limiter"] = (f"FP32 FMA pipe + shared-memory exchange (~{lane_ops / 1e3:.0f}k FP32 "
+                          "lane ops per row; ncu: FP32 pipe 67%, issue 55% at w = 128)")
     return out
 
 
