@@ -327,8 +327,11 @@ def test_config3_full_scale_vs_oracle(hh):
 @pytest.mark.parametrize("n_el,n_f,upsample,b0,w", [(37, 256, 4, 80, 96), (9, 512, 4, 0, 64),
                                                     (5, 1024, 4, 4000, 96), (3, 128, 8, 300, 211),
                                                     (4, 64, 4, 17, 239),
-                                                    (2000, 1024, 4, 49, 288),   # config 4 rows, its gate
-                                                    (3000, 512, 4, 0, 352),     # config 3 rows, its gate
+                                                    (2000, 1024, 4, 49, 288),   # config 4 rows, box gate
+                                                    (3000, 512, 4, 0, 352),     # config 3 rows, box gate
+                                                    (2000, 1024, 4, 65, 128),   # config 4, near-band gate
+                                                    (3000, 512, 4, 10, 64),     # config 3, near-band gate
+                                                    (70, 1024, 4, 63, 129), (70, 1024, 4, 1, 255),
                                                     # 4096-bin rows, gated: the one-exchange kernel
                                                     (300, 1024, 4, 0, 512), (300, 1024, 4, 3584, 512),
                                                     (70, 1024, 4, 4095, 1), (70, 1024, 4, 63, 65),
