@@ -445,6 +445,44 @@ def test_public_api_host_input_forms():
         assert o.provenance == outs[0].provenance
 
 
+def test_gate_miss_redoes_on_full_profiles(monkeypatch):
+    """A leaf delay outside the range gate (forced here by shifting the
+    gated window up by half its width) makes hhffbpa_reconstruct redo the
+    step on full profiles: the result is the ungated step's, bit for bit,
+    with the same provenance -- never a volume missing contributions."""
+    import paper_2506_23568_b200 as hh
+    from paper_2506_23568_b200 import ffbp, rangecomp, workloads
+    w = workloads.config(2, frames=512)
+    cube = workloads.simulate_numpy(w)
+    params = hh.FfbpParams(levels=7)
+    dims = (48, 48, 16)
+    want = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4, merge_factor=4)
+    orig_win, orig_full = rangecomp.range_compress_window, rangecomp.range_compress_device
+    calls = {"window": 0, "full": 0}
+
+    def shifted(cube_dev, kgrid, upsample, b0, width, **kw):
+        calls["window"] += 1
+        return orig_win(cube_dev, kgrid, upsample, b0 + width // 2, width - width // 2, **kw)
+
+    def full(*a, **kw):
+        calls["full"] += 1
+        return orig_full(*a, **kw)
+
+    monkeypatch.setattr(rangecomp, "range_compress_window", shifted)
+    monkeypatch.setattr(rangecomp, "range_compress_device", full)
+    got = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4, merge_factor=4)
+    assert calls["window"] >= 1 and calls["full"] == 1  # the gate missed: one ungated redo
+    monkeypatch.undo()
+    import torch
+    el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
+    cube_dev = torch.as_tensor(np.asarray(cube.values), device="cuda")
+    ungated = ffbp.hhffbpa_from_cube(cube_dev, el, hh.bpa.el_f32x4(el), w.freqs, w.region, dims,
+                                     params, 7, 4, 4, gate=False)
+    assert np.array_equal(got.values, ungated.volume.cpu().numpy().reshape(dims))
+    assert got.provenance == want.provenance
+    assert rel_l2(got.values, want.values) < 1e-5
+
+
 def test_reconstruct_stream_equals_single_calls():
     """hhffbpa_reconstruct_stream (uploads overlapped across volumes, plan
     cache from the first volume) returns, per cube, exactly what
