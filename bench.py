@@ -426,6 +426,7 @@ def run_ours(args):
         res["configs"]["1"] = bpa_leg(dev, args)
         c3, detail["config3"], c3_host = hhffbpa_small_leg(3, dev, args)
         c2, detail["config2"], _ = hhffbpa_small_leg(2, dev, args)
+        c2["leaf_sweep"], detail["config2_leaf_sweep"] = leaf_sweep_leg(dev, args)
         res["configs"]["3"], res["configs"]["2"] = c3, c2
     # CPU legs: headline parity (oracle), the reference's CPU baseline, and
     # the reference's own full config-3 run (+ GPU-vs-reference parity)
@@ -786,6 +787,43 @@ def hhffbpa_small_leg(index, dev, args):
     del cube, graph
     torch.cuda.empty_cache()
     return out, detail, (w, host, vol, e2e_s)
+
+
+def leaf_sweep_leg(dev, args):
+    """BASELINE config 2's sweep: HHFFBPA with merge factor 4 and leaves of
+    8 / 16 / 32 frames (2^(M-1) balanced leaves of the 4,000 x 8 element
+    aperture, M = 10 / 9 / 8), each against direct BPA on the same cube --
+    the accuracy / speed trade-off: graph-replayed device step, complex
+    rel-L2 and psnr (GPU metrics) against the BPA volume.  Returns (compact
+    {frames: [ms, rel-L2, psnr dB]}, detail)."""
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, ffbp, metrics, rangecomp, workloads
+    w = workloads.config(2)
+    el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+    cube = _native.simulate_uniform(el, w.scene_pos, w.scene_refl, w.freqs)
+    el4 = bpa.el_f32x4(el)
+    env, dt, k_ref = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
+    ref, _ = bpa.bpa_volume_device(env, el4, w.region, w.dims, 0.0, dt, k_ref)
+    del env
+    torch.cuda.synchronize()
+    compact, detail = {}, {"workload": "BASELINE config 2 sweep: merge factor 4, leaves of "
+                                       "8/16/32 frames (M = 10/9/8) vs direct BPA, same cube",
+                           "columns": ["ms_per_step", "rel_l2_vs_bpa", "psnr_vs_bpa_db"]}
+    for frames, levels in ((8, 10), (16, 9), (32, 8)):
+        params = ffbp.FfbpParams(levels=levels)
+        graph = ffbp.StepGraph(cube, el, el4, w.freqs, w.region, w.dims, params, levels, 4,
+                               w.upsample)
+        ms, _, last = _timed_steps(graph.replay, max(args.steps, 20), max(args.warmup, 3))
+        v = last.volume
+        rel = (torch.linalg.norm(v - ref) / torch.linalg.norm(ref)).item()
+        compact[str(frames)] = [round(ms, 3), round(rel, 4), round(metrics.psnr_device(ref, v), 2)]
+        detail[f"leaf_{frames}_frames"] = {"levels": levels,
+                                           "leaf_elements": int(w.n_elements >> (levels - 1)),
+                                           "volumes_per_s": round(1e3 / ms, 1)}
+        del graph, last, v
+    del cube, ref
+    torch.cuda.empty_cache()
+    return compact, detail
 
 
 def reference_leg_config3(out, held):
