@@ -390,6 +390,9 @@ def run_ours(args):
 
     # ---- e2e through the public API, host buffers --------------------------
     e2e, e2e_detail = e2e_leg(args, w, params, cube, e0, e1, world, rank, dev)
+    # N ranks: the sharded config 3 / config 1 legs need every rank
+    sharded = (sharded_legs(dev, args, comm, world, rank, barrier)
+               if world > 1 and not args.no_extra else None)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -421,6 +424,8 @@ def run_ours(args):
     # threads left spinning by OpenMP / Numba would perturb the
     # host-orchestrated sub-3 ms steps of configs 2 / 3
     cpu_rows = cube[: 16 * 1024 * 128] if world == 1 and not args.no_cpu_baseline else None
+    if world > 1 and sharded is not None:
+        res["configs"] = sharded
     if world == 1 and not args.no_extra:
         res["configs"] = {}
         res["configs"]["1"] = bpa_leg(dev, args)
@@ -742,6 +747,57 @@ def bpa_leg(dev, args):
     return {"bpa_gunits_per_s": round(units / ms / 1e6, 1), "ms": round(ms, 3),
             "roofline": {"kernel": "bpa_tile_kernel", "bound": "sfu", "achieved": round(ach, 1),
                          "peak": round(peak, 1), "frac": round(ach / peak, 4)}}
+
+
+def sharded_legs(dev, args, comm, world, rank, barrier):
+    """N ranks: BASELINE config 3 HHFFBPA (subaperture-group sharded, as the
+    headline, output "shard") and config 1 direct BPA (voxel slabs, every
+    rank compressing the whole 32,000-element cube, no gather) -- the other
+    two configs BASELINE scales at 1/2/4/8 GPUs; device step, max over
+    ranks (rank 0's summary)."""
+    import torch
+    from paper_2506_23568_b200 import _native, bpa, dist as hdist, ffbp, rangecomp, workloads
+    out = {}
+    w = workloads.config(3)
+    params = ffbp.FfbpParams(levels=w.levels)
+    el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+    e0, e1 = hdist.plan_shard(w.n_elements, w.levels, w.merge_factor, world, rank)[3]
+    cube = _native.simulate_uniform(el[e0:e1], w.scene_pos, w.scene_refl, w.freqs)
+    plan = {}
+
+    def step3():
+        r = hdist.hhffbpa_sharded_device(comm, cube, e0, el, w.freqs, w.region, w.dims, params,
+                                         w.levels, w.merge_factor, w.upsample, output="shard",
+                                         plan_cache=plan.get("plan"))
+        plan.setdefault("plan", r.plan)
+        return r
+
+    ms, _, last = _timed_steps(step3, max(args.steps, 20), max(args.warmup, 3), barrier)
+    assert int(last.oow.cpu()[0]) == 0
+    ms, = _max_over_ranks([ms], world)
+    out["3"] = {"ms": round(ms, 3), "value": round(w.bpa_units / (ms / 1e3) / 1e9, 1),
+                "parallelism": f"subaperture groups + voxel slabs x{world}"}
+    del cube, last, plan
+    w = workloads.config(1)
+    el = torch.tensor(np.asarray(w.aperture.elements), device=dev)
+    cube = _native.simulate_uniform(el, w.scene_pos, w.scene_refl, w.freqs)
+    el4 = bpa.el_f32x4(el)
+    n_t, dt, k_ref, _ = rangecomp.profile_axis(w.freqs, w.upsample)
+    vb, ve = hdist.shard_range(w.n_voxels, rank, world)
+    oow = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def step1():
+        env, _, _ = rangecomp.range_compress_device(cube, w.freqs, w.upsample)
+        return bpa.bpa_volume_device(env, el4, w.region, w.dims, 0.0, dt, k_ref,
+                                     vox_range=(vb, ve), oow=oow)
+
+    ms, _, _ = _timed_steps(step1, args.steps, args.warmup, barrier)
+    ms, = _max_over_ranks([ms], world)
+    out["1"] = {"bpa_gunits_per_s": round(float(w.n_voxels) * w.n_elements / ms / 1e6, 1),
+                "ms": round(ms, 3), "parallelism": f"voxel slabs x{world}"}
+    del cube
+    torch.cuda.empty_cache()
+    return out
 
 
 def hhffbpa_small_leg(index, dev, args):
