@@ -380,7 +380,7 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     """
     import torch
     from .bpa import el_f32x4
-    from .ffbp import (NEWTON_FIRST_MAX_COLUMNS, Pipeline, PlanCache, finish_lattices,
+    from .ffbp import (Pipeline, PlanCache, finish_lattices,
                        geometry_stream, plan_lattices, src_pad_of)
     from .rangecomp import profile_axis, range_compress_device, range_compress_window
     world, rank = comm.world, comm.rank
@@ -410,9 +410,8 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         if plan_cache is None:
             pending["done"].synchronize()
         n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
-        if n_cols <= NEWTON_FIRST_MAX_COLUMNS or upload is not None:
-            with torch.cuda.stream(geo):
-                lat = finish_lattices(pending, newton_grids=mask)
+        with torch.cuda.stream(geo):  # Newton first, as the 1-GPU step (ffbp)
+            lat = finish_lattices(pending, newton_grids=mask)
         env, t0, dt, k_ref = range_compress_window(
             cube_dev_rows, kgrid, upsample, b0, w, chunks=upload.chunks if upload else None,
             row0=e_row0)
