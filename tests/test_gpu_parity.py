@@ -356,8 +356,11 @@ def test_range_compress_window_equals_full_slice(n_el, n_f, upsample, b0, w):
     assert rel_l2(got.cpu().numpy(), want.cpu().numpy()) < 2e-6
 
 
-@pytest.mark.parametrize("config", [2, 3, 4])
-def test_range_gate_matches_full_profiles(config):
+@pytest.mark.parametrize("config,levels,kernel", [(2, None, "linear"), (3, None, "linear"),
+                                                 (4, None, "linear"),
+                                                 (2, 6, "cubic"),    # 1,000-element leaves
+                                                 (3, 8, "linear")])  # 1,024-element leaves
+def test_range_gate_matches_full_profiles(config, levels, kernel):
     """HHFFBPA with range-gated compression (only the delay bins the leaf
     stage can read, ffbp.leaf_range_gate) equals the run on full profiles:
     same image to float rounding, same lattices and flags, no leaf delay
@@ -370,9 +373,10 @@ def test_range_gate_matches_full_profiles(config):
                        generator=gen)
     el = torch.tensor(np.asarray(w.aperture.elements), device="cuda")
     el4 = bpa.el_f32x4(el)
-    params = ffbp.FfbpParams(levels=w.levels)
-    # config 4: full profiles 68.7 GB + cube 17.2 GB (+ 4.8 GB gated)
-    runs = [ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params, w.levels,
+    levels = levels or w.levels
+    params = ffbp.FfbpParams(levels=levels, kernel=kernel)
+    # config 4: full profiles 68.7 GB + cube 17.2 GB (+ 2.1 GB gated)
+    runs = [ffbp.hhffbpa_from_cube(cube, el, el4, w.freqs, w.region, w.dims, params, levels,
                                    w.merge_factor, w.upsample, gate=g) for g in (False, True)]
     torch.cuda.synchronize()
     del cube
