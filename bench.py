@@ -603,13 +603,24 @@ def rc_roofline(w, run, rc_ms, step_ms):
                            "peak_tflops": round(fp32 / 1e12, 1),
                            "frac": round(flops / (kms / 1e3) / fp32, 3)}
     out["traffic"] = _traffic(kname + "_config4")  # profiles/traffic.json
-    if split:
+    if split and n_t == 4096:
         # what actually limits it (profiles/r02_config4_ncu.txt): the FP32
-        # pipe, not HBM -- the contract's bound field has no FP32 option
+        # pipe, not HBM (the contract's bound field has no FP32 option).
+        # FP32 lane operations per row, counted from the kernel's arithmetic:
+        # stage A, per 64 columns four 16-point DFTs (168) and 45 twiddle
+        # products (4 each); stage B, per thread and slice b three twiddle
+        # products, the 4-point DFT's outputs in use (12 for <= 2 bins, else
+        # 16) and one 4-FMA Horner step per bin (ncu at w = 128: 87.4 k)
         c = -(-gw // 64)
-        lane_ops = (54.5 if n_t == 4096 else 27.0) * 1e3 + 64 * 16 * (28 + 4 * c)
-        out["limiter"] = (f"FP32 FMA pipe + shared-memory exchange (~{lane_ops / 1e3:.0f}k FP32 "
-                          "lane ops per row; ncu: FP32 pipe 67%, issue 55% at w = 128)")
+        lane_ops = 64 * (4 * 168 + 45 * 4) + 64 * 16 * (12 + (12 if c <= 2 else 16) + 4 * c)
+        peak32 = 148 * 128 * _sm_clock() * 1e6
+        if kms:
+            ach32 = lane_ops * w.n_elements / (kms / 1e3)
+            out["fp32"] = {"achieved": round(ach32 / 1e12, 2), "peak": round(peak32 / 1e12, 2),
+                           "unit": "T FP32 lane-ops/s", "frac": round(ach32 / peak32, 3),
+                           "lane_ops_per_row": lane_ops}
+        out["limiter"] = ("FP32 FMA pipe + shared-memory exchange (ncu at w = 128: FP32 pipe "
+                          "67%, issue 55%; the HBM floor is below the FP32 floor)")
     return out
 
 
