@@ -703,10 +703,10 @@ extern "C" int hhsar_range_compress_window(const void *cube, int64_t n_el, int64
             roots.w[m] = make_float2((float)cos(ph), (float)sin(ph));
             roots.iw[m] = make_float2(-roots.w[m].y, roots.w[m].x);
         }
-        for (int o = 0; o < 8; ++o) {  // e^{j a dt 64 o}, reduced like cis_reduced
-            const double rev = a * (dt * 64.0 * (double)o) / (2.0 * M_PI);
+        for (int q = 0; q < 8; ++q) {  // e^{j a dt 64 q}, reduced like cis_reduced
+            const double rev = a * (dt * 64.0 * (double)q) / (2.0 * M_PI);
             const double red = 2.0 * M_PI * (rev - nearbyint(rev));
-            roots.dstep[o] = make_float2((float)cos(red), (float)sin(red));
+            roots.dstep[q] = make_float2((float)cos(red), (float)sin(red));
         }
         const int gb = (int)b0, gw = (int)w;
         if (split4096)
