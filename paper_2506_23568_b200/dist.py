@@ -252,7 +252,7 @@ def owned_elements(n_elements: int, levels: int, merge_factor: int = 2, comm=Non
 
 def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsample: int = 8,
                                 merge_factor: int = 2, comm=None, output: str = "all",
-                                rows=None):
+                                rows=None, split_top: bool = False):
     """hhffbpa_reconstruct (ffbp.py:415-513) over all ranks of `comm`
     (default: torch.distributed's world).  Each rank transfers and
     range-compresses only its own subaperture group's echoes (streamed in
@@ -269,6 +269,8 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
     ``rows``: this rank's echo rows [e0, e1) only (owned_elements()), e.g.
     a pinned host buffer each process filled itself; ``cube.values`` is then
     never read (each process holds 1/W of the cube).
+    ``split_top``: see hhffbpa_sharded_device (the top grids' Newton split by
+    u-rows across ranks instead of run whole on every rank).
     """
     import torch
     from .bpa import _finish, check_delay_window, default_grid_dims, region_grid
@@ -317,11 +319,11 @@ def hhffbpa_reconstruct_sharded(cube, region, final_dims=None, params=None, upsa
 
     res = hhffbpa_sharded_device(comm, None, e0, el_dev, kgrid, region, dims, params,
                                  levels, merge_factor, upsample, output=output,
-                                 upload=start_upload)
+                                 upload=start_upload, split_top=split_top)
     if int(res.oow.cpu()[0]):  # a leaf delay outside the range gate (all-reduced: every rank agrees)
         res = hhffbpa_sharded_device(comm, uploads[0].tensor, e0, el_dev, kgrid, region, dims,
                                      params, levels, merge_factor, upsample, gate=False,
-                                     output=output)
+                                     output=output, split_top=split_top)
     origin, step = region_grid(region, dims)
     extra = torch.cat([res.flags, res.stats.reshape(-1)])
     whole = output == "all" or (output == "root" and comm.rank == 0)
@@ -352,7 +354,7 @@ class ShardedVolume(SimpleNamespace):
 def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, region, final_dims,
                            params, levels: int, merge_factor: int, upsample: int,
                            gate: bool = True, output: str = "all", upload=None,
-                           plan_cache=None):
+                           plan_cache=None, split_top: bool = False):
     """One rank's share of HHFFBPA:
 
     1. subaperture-group partition: the rank owns a contiguous run of
@@ -368,6 +370,11 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
     4. the Cartesian landing voxel-sharded, then (``output``) an all-gather
        of the slabs ("all"), a gather to rank 0 ("root") or nothing
        ("shard").
+
+    ``split_top``: the grids above the exchange level (planned and merged
+    by every rank) are inverted split by lattice u-rows across the ranks
+    (grid build) and their positions / masks / counters summed
+    with one all-reduce, instead of every rank inverting them whole.
 
     ``upload`` (rangecomp.CubeUpload of this rank's rows, or a zero-argument
     factory of one started right after the plan is queued; ``cube_dev_rows``
@@ -392,6 +399,9 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         mask[a:b] = True
     n_t, dt, _, _ = profile_axis(kgrid, upsample)
     window_hi = (n_t - 1) * dt
+    g_top = sched.level_slices[kx][1] if kx >= 0 else sched.n_grids  # first grid above
+    split_top = bool(split_top) and world > 1 and kx >= 0 and g_top < sched.n_grids
+    row_split = (rank, world, range(g_top, sched.n_grids)) if split_top else None
     # as ffbp.hhffbpa_from_cube: plan and Newton on the high-priority
     # geometry stream, the (gated) range compression on the caller's stream
     # beside Newton
@@ -411,7 +421,7 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
             pending["done"].synchronize()
         n_cols, b0, w = (int(v) for v in pending["host_s"][16:40].view(np.int64))
         with torch.cuda.stream(geo):  # Newton first, as the 1-GPU step (ffbp)
-            lat = finish_lattices(pending, newton_grids=mask)
+            lat = finish_lattices(pending, newton_grids=mask, row_split=row_split)
         env, t0, dt, k_ref = range_compress_window(
             cube_dev_rows, kgrid, upsample, b0, w, chunks=upload.chunks if upload else None,
             row0=e_row0)
@@ -422,8 +432,22 @@ def hhffbpa_sharded_device(comm, cube_dev_rows, e_row0: int, el_dev, kgrid, regi
         t0 = 0.0
     if lat is None:
         with torch.cuda.stream(geo):
-            lat = finish_lattices(pending, newton_grids=mask)
+            lat = finish_lattices(pending, newton_grids=mask, row_split=row_split)
     main.wait_stream(geo)
+    if split_top:
+        # each top-grid point was inverted by exactly one rank: sum the
+        # shares (the positions pool is uninitialised where a rank did not
+        # invert, so every rank zeroes the rows it left to the others first
+        # -- on the geometry stream, ahead of nothing: Newton has run)
+        p0 = int(lat.descs["offset"][g_top])
+        p1 = int(lat.descs["offset"][-1] + lat.npts[-1])
+        top_pos = lat.positions[p0:p1]
+        own = lat.valid[p0:p1] != 0
+        top_pos.mul_(own.unsqueeze(1).to(top_pos.dtype))
+        comm.allreduce_sum(top_pos)
+        comm.allreduce_sum(lat.valid[p0:p1])
+        top_stats = lat.stats[g_top:]
+        comm.allreduce_sum(top_stats)
     for t in (lat.positions, lat.valid, lat.stats, lat.keep[1]):
         t.record_stream(main)
     pipe = Pipeline(env, el_dev, el_f32x4(el_dev), t0, dt, k_ref, kgrid, region, final_dims,

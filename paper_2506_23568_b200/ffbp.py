@@ -335,8 +335,14 @@ def plan_lattices(el_dev, sched: Schedule, region, kgrid, gamma: float, margin: 
 _trace = None  # optional host-timeline hook (tools/host_overhead.py)
 
 
-def finish_lattices(p, newton_grids=None) -> Lattices:
-    """Wait for the plan, size the pools, launch Newton (current stream)."""
+def finish_lattices(p, newton_grids=None, row_split=None) -> Lattices:
+    """Wait for the plan, size the pools, launch Newton (current stream).
+
+    ``row_split`` = (rank, world, grids) with ``newton_grids``: of each listed
+    grid this process inverts only its share of the active rectangle's
+    u-rows (rows [lo + n r / W, lo + n (r + 1) / W)); a column's planes are
+    solved in order within the column only, so the union over ranks is the
+    full inversion (dist.hhffbpa_sharded_device sums the shares)."""
     import torch
     cached = p.get("cached")
     if cached is None:
@@ -368,6 +374,14 @@ def finish_lattices(p, newton_grids=None) -> Lattices:
     elif newton_grids is not None:
         # Newton work list restricted to the selected grids: re-derive the
         # column offsets and send the descriptors back up
+        if row_split is not None:
+            r, world, gl = row_split
+            for g in gl:
+                lo, hi = int(host["act_lo"][g, 0]), int(host["act_hi"][g, 0])
+                n = hi - lo + 1
+                if n > 0:
+                    host["act_lo"][g, 0] = lo + n * r // world
+                    host["act_hi"][g, 0] = lo + n * (r + 1) // world - 1
         span = np.maximum(host["act_hi"].astype(np.int64) - host["act_lo"] + 1, 0)
         cols = np.where(np.asarray(newton_grids, dtype=bool), span[:, 0] * span[:, 1], 0)
         starts = np.cumsum(cols)

@@ -44,8 +44,15 @@ def case():
     return w, cube
 
 
-@pytest.mark.parametrize("world,levels,factor", [(2, 7, 2), (4, 7, 2), (3, 6, 2), (2, 7, 4)])
-def test_sharded_hhffbpa_equals_single_gpu(case, world, levels, factor):
+@pytest.mark.parametrize("world,levels,factor,split_top", [(2, 7, 2, False), (4, 7, 2, False),
+                                                           (3, 6, 2, False), (2, 7, 4, False),
+                                                           (4, 7, 2, True), (3, 6, 2, True),
+                                                           (2, 7, 4, True)])
+def test_sharded_hhffbpa_equals_single_gpu(case, world, levels, factor, split_top):
+    """The sharded HHFFBPA equals the single-GPU run at W = 2/3/4, binary
+    and factor 4 -- also with the top grids' Newton split by u-rows across
+    the ranks (split_top): the summed shares are the whole inversion, so
+    volume and provenance (per-grid counts, flags) are unchanged."""
     import paper_2506_23568_b200 as hh
     from paper_2506_23568_b200.dist import hhffbpa_reconstruct_sharded
     w, cube = case
@@ -54,7 +61,8 @@ def test_sharded_hhffbpa_equals_single_gpu(case, world, levels, factor):
     single = hh.hhffbpa_reconstruct(cube, w.region, dims, params, upsample=4,
                                     merge_factor=factor)
     outs = _run_world(world, lambda comm: hhffbpa_reconstruct_sharded(
-        cube, w.region, dims, params, upsample=4, merge_factor=factor, comm=comm))
+        cube, w.region, dims, params, upsample=4, merge_factor=factor, comm=comm,
+        split_top=split_top))
     for vol in outs:
         err = np.linalg.norm(vol.values - single.values) / np.linalg.norm(single.values)
         assert err < 1e-6, err

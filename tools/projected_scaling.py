@@ -9,7 +9,8 @@ rank's device time + exchange bytes / bandwidth.
     python tools/projected_scaling.py 3 2 4 8     (config, worlds...)
     OUTPUT=all|root|shard python tools/projected_scaling.py 4 2 4 8
       (volume output mode of dist.hhffbpa_sharded_device; default shard,
-      the bench's N > 1 mode; CACHED=0: no per-rank plan cache)
+      the bench's N > 1 mode; CACHED=0: no per-rank plan cache; SPLIT_TOP=1:
+      the top grids' Newton split by u-rows across ranks + one all-reduce)
 """
 import os
 import json
@@ -48,6 +49,7 @@ class CountingComm:
 
 OUTPUT = os.environ.get("OUTPUT", "shard")
 CACHED = os.environ.get("CACHED", "1") == "1"  # per-rank plan cache (the bench's N > 1 step)
+SPLIT_TOP = os.environ.get("SPLIT_TOP", "0") == "1"
 
 
 def time_rank(w, cube, el, params, factor, world, rank, reps=3):
@@ -61,7 +63,8 @@ def time_rank(w, cube, el, params, factor, world, rank, reps=3):
         # as the bench's N-rank step: the first call's plan is cached
         r = dist.hhffbpa_sharded_device(comm, rows, e0, el, w.freqs, w.region, w.dims, params,
                                         w.levels, factor, w.upsample, output=OUTPUT,
-                                        plan_cache=plan if CACHED else None)
+                                        plan_cache=plan if CACHED else None,
+                                        split_top=SPLIT_TOP)
         plan = r.plan
         e.record()
         torch.cuda.synchronize()
@@ -83,7 +86,7 @@ def main():
     params = ffbp.FfbpParams(levels=w.levels)
     t1, _ = time_rank(w, cube, el, params, factor, 1, 0)
     out = {"config": cfg, "merge_factor": factor, "one_gpu_ms": round(t1, 3),
-           "nvlink_gbs_assumed": NVLINK_GBS, "output": OUTPUT, "note": "projection: ranks timed one at a time "
+           "nvlink_gbs_assumed": NVLINK_GBS, "output": OUTPUT, "split_top": SPLIT_TOP, "note": "projection: ranks timed one at a time "
            "on one B200, collectives costed from bytes", "worlds": {}}
     for W in worlds:
         per = [time_rank(w, cube, el, params, factor, W, r) for r in range(W)]
