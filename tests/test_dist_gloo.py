@@ -74,10 +74,20 @@ def _comm_worker(rank, world, port, out_path):
     comm.allgather_segments(buf, segs)
     cnt = torch.tensor([rank + 1, 10 * rank], dtype=torch.int64)
     comm.allreduce_sum(cnt)
+    # split_top's sums: uint8 masks and float64 positions, each point owned by
+    # one rank (the others hold zeros), on views into larger pools
+    pool_v = torch.zeros(12, dtype=torch.uint8)
+    pool_p = torch.zeros((12, 3), dtype=torch.float64)
+    mine = torch.arange(12) % world == rank
+    pool_v[4:][mine[4:]] = 1
+    pool_p[4:][mine[4:]] = torch.arange(8, dtype=torch.float64)[mine[4:]].unsqueeze(1) + 0.25
+    comm.allreduce_sum(pool_v[4:])
+    comm.allreduce_sum(pool_p[4:])
     # the subtree plan every rank derives must tile the leaves / elements
     plans = [plan_shard(1000, 8, 2, world, r) for r in range(world)]
     if rank == 0:
         np.save(out_path, {"buf": buf.numpy(), "root": root_buf.numpy(), "cnt": cnt.numpy(),
+                           "pool_v": pool_v.numpy(), "pool_p": pool_p.numpy(),
                            "rows": [p[3] for p in plans], "kx": [p[1] for p in plans]},
                 allow_pickle=True)
     dist.barrier()
@@ -94,6 +104,9 @@ def test_comm_segments_allreduce_and_plan(tmp_path, world):
     assert np.array_equal(res["buf"], np.arange(n) * (1 + 1j))
     assert np.array_equal(res["root"], np.arange(n) * (1 + 1j))
     assert list(res["cnt"]) == [sum(range(1, world + 1)), 10 * sum(range(world))]
+    assert list(res["pool_v"]) == [0] * 4 + [1] * 8
+    assert np.array_equal(res["pool_p"][4:], np.repeat(np.arange(8.0)[:, None] + 0.25, 3, 1))
+    assert not res["pool_p"][:4].any()
     rows = res["rows"]
     assert rows[0][0] == 0 and rows[-1][1] == 1000
     assert all(rows[r][1] == rows[r + 1][0] for r in range(world - 1))
