@@ -611,8 +611,7 @@ def rc_roofline(w, run, rc_ms, step_ms):
         # products (4 each); stage B, per thread and slice b three twiddle
         # products, the 4-point DFT's outputs in use (12 for <= 2 bins, else
         # 16) and one 4-FMA Horner step per bin (ncu at w = 128: 87.4 k)
-        c = -(-gw // 64)
-        lane_ops = 64 * (4 * 168 + 45 * 4) + 64 * 16 * (12 + (12 if c <= 2 else 16) + 4 * c)
+        lane_ops = rc_lane_ops(n_t, w.freqs.count, gw)
         peak32 = 148 * 128 * _sm_clock() * 1e6
         if kms:
             ach32 = lane_ops * w.n_elements / (kms / 1e3)
@@ -650,8 +649,14 @@ def hhffbpa_roofline(w, run, ms):
     n_t = w.freqs.count * w.upsample
     gw = run.lattices.gate[1] if run.lattices.gate else n_t
     it = int(stats[:, 4].sum())
+    rc_bytes = w.n_elements * (w.freqs.count + gw) * 8 / hbm
+    # the compression's FP32 work where it is counted (the split kernels of
+    # 4,096 / 2,048-bin rows, rc_lane_ops): SURVEY 8(d) takes the max of a
+    # stage's bounds, and this stage's FP32 floor is above its HBM floor
+    lane_ops = rc_lane_ops(n_t, w.freqs.count, gw)
+    rc_fp32 = w.n_elements * lane_ops / (128 * sms * clk) if lane_ops else 0.0
     stages = {
-        "range_compression": w.n_elements * (w.freqs.count + gw) * 8 / hbm,
+        "range_compression": max(rc_bytes, rc_fp32),
         "newton": it * 150 / (64 * sms * clk),
         "leaf": leaf_units * 3 / (16 * sms * clk),
         "merges": merge_units * 45 / (64 * sms * clk),
@@ -662,8 +667,24 @@ def hhffbpa_roofline(w, run, ms):
             "stages_ms": {k: round(v * 1e3, 3) for k, v in stages.items()},
             "work": {"leaf_units": leaf_units, "merge_units": merge_units,
                      "landing_units": landing_units, "newton_iterations": it},
-            "method": "SURVEY 8(d): HBM bytes / measured HBM, Newton 150 FP64 instr, leaf 3 "
-                      "MUFU, merge/landing 45 FP64 instr per unit"}
+            "method": "SURVEY 8(d): compression max(HBM bytes / measured HBM, counted FP32 "
+                      "lane ops / FP32 peak), Newton 150 FP64 instr, leaf 3 MUFU, "
+                      "merge/landing 45 FP64 instr per unit"}
+
+
+def rc_lane_ops(n_t, n_f, gw):
+    """FP32 lane operations per row of the split range compression (None
+    where another kernel runs): stage A, per 64 columns the residue DFTs of
+    the column's live samples (16-point: 168 lane ops, 8-point: 56) and their
+    input twiddles (4 per product); stage B, per thread and 16-row slice b
+    three twiddle products, the small DFT's outputs in use and one 4-FMA
+    Horner step per bin (ncu at config 4, w = 128: 87.4 k)."""
+    c = -(-gw // 64)
+    if n_t == 4096 and n_f == 1024 and gw <= 512:
+        return 64 * (4 * 168 + 45 * 4) + 64 * 16 * (12 + (12 if c <= 2 else 16) + 4 * c)
+    if n_t == 2048 and n_f == 512 and gw <= 512:
+        return 64 * (4 * 56 + 21 * 4) + 64 * 16 * (12 + (4 if c <= 1 else 8) + 4 * c)
+    return None
 
 
 def parity_leg(w, run):
