@@ -576,10 +576,15 @@ def _h2d_probe(host):
 def rc_roofline(w, run, rc_ms, step_ms):
     """Dominant kernel of the config-4 step: the range-gated compression
     (range_compress_split_kernel for 4,096- / 2,048-bin rows and a window of
-    <= 512 bins, else range_compress_kernel).  Algorithmic bytes per launch = the cube read
-    once (N_el x n_f x 8 B) + the gated envelopes written once (N_el x w x 8
-    B); also reported against the FFT's FP32 work."""
-    from paper_2506_23568_b200 import ffbp, rangecomp
+    <= 512 bins, else range_compress_kernel), against the unit that bounds
+    it.  The split kernel is FP32-bound: its counted FP32 lane operations
+    per row (rc_lane_ops; ncu's pipe counters agree) need more time at the
+    FP32 peak (148 SMs x 128 lanes x clock) than its bytes need at the
+    measured HBM bandwidth, so `bound` is "fp32" with the HBM reading in
+    `hbm` (algorithmic bytes per launch: the cube read once, N_el x n_f x 8
+    B, plus the gated envelopes written once, N_el x w x 8 B); the other
+    kernel is reported against HBM.  `traffic`: ncu DRAM bytes per launch."""
+    from paper_2506_23568_b200 import rangecomp
     n_t, dt, _, _ = rangecomp.profile_axis(w.freqs, w.upsample)
     b0, gw = run.lattices.gate
     by = w.n_elements * (w.freqs.count + gw) * 8.0
@@ -588,38 +593,25 @@ def rc_roofline(w, run, rc_ms, step_ms):
     split = ((n_t == 4096 and w.freqs.count in (512, 1024)) or
              (n_t == 2048 and w.freqs.count in (256, 512))) and gw <= 512
     kname = "range_compress_split_kernel" if split else "range_compress_kernel"
-    out = {"kernel": kname, "bound": "hbm", "unit": "GB/s", "peak": peak,
-           "algorithmic_bytes": int(by), "gate": [b0, gw, n_t]}
+    lane_ops = rc_lane_ops(n_t, w.freqs.count, gw) if split else None
+    hbm = {"peak": peak, "unit": "GB/s", "algorithmic_bytes": int(by)}
+    out = {"kernel": kname, "gate": [b0, gw, n_t]}
     if kms:
         ach = by / (kms / 1e3) / 1e9
-        out.update(achieved=round(ach, 1), frac=round(ach / peak, 4), kernel_ms=round(kms, 3),
-                   share_of_step=round(kms / step_ms, 3))
-        # FFT work: radix-2-equivalent 5 n log2 n flops per row of the padded
-        # transform (the kernel prunes the zero padding and the unneeded
-        # outputs of the last pass), vs 148 SMs x 128 FP32 lanes x 2 x clock
-        flops = w.n_elements * 5.0 * n_t * np.log2(n_t)
-        fp32 = 148 * 128 * 2 * _sm_clock() * 1e6
-        out["fft_fp32"] = {"tflops": round(flops / (kms / 1e3) / 1e12, 1),
-                           "peak_tflops": round(fp32 / 1e12, 1),
-                           "frac": round(flops / (kms / 1e3) / fp32, 3)}
-    out["traffic"] = _traffic(kname + "_config4")  # profiles/traffic.json
-    if split and n_t == 4096:
-        # what actually limits it (profiles/r02_config4_ncu.txt): the FP32
-        # pipe, not HBM (the contract's bound field has no FP32 option).
-        # FP32 lane operations per row, counted from the kernel's arithmetic:
-        # stage A, per 64 columns four 16-point DFTs (168) and 45 twiddle
-        # products (4 each); stage B, per thread and slice b three twiddle
-        # products, the 4-point DFT's outputs in use (12 for <= 2 bins, else
-        # 16) and one 4-FMA Horner step per bin (ncu at w = 128: 87.4 k)
-        lane_ops = rc_lane_ops(n_t, w.freqs.count, gw)
+        hbm.update(achieved=round(ach, 1), frac=round(ach / peak, 4))
+    if lane_ops:
         peak32 = 148 * 128 * _sm_clock() * 1e6
+        out.update(bound="fp32", unit="T FP32 lane-ops/s", peak=round(peak32 / 1e12, 2),
+                   lane_ops_per_row=lane_ops)
         if kms:
             ach32 = lane_ops * w.n_elements / (kms / 1e3)
-            out["fp32"] = {"achieved": round(ach32 / 1e12, 2), "peak": round(peak32 / 1e12, 2),
-                           "unit": "T FP32 lane-ops/s", "frac": round(ach32 / peak32, 3),
-                           "lane_ops_per_row": lane_ops}
-        out["limiter"] = ("FP32 FMA pipe + shared-memory exchange (ncu at w = 128: FP32 pipe "
-                          "67%, issue 55%; the HBM floor is below the FP32 floor)")
+            out.update(achieved=round(ach32 / 1e12, 2), frac=round(ach32 / peak32, 3))
+        out["hbm"] = hbm
+    else:
+        out.update(bound="hbm", **{k: v for k, v in hbm.items()})
+    if kms:
+        out.update(kernel_ms=round(kms, 3), share_of_step=round(kms / step_ms, 3))
+    out["traffic"] = _traffic(kname + "_config4")  # profiles/traffic.json
     return out
 
 
